@@ -1,0 +1,370 @@
+#!/usr/bin/env python
+"""Benchmark of the per-block chaotic operation mode (arXiv 1201.3114) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload c4|c3]
+    python -m torch.distributed.run --nnodes=1 --nproc-per-node N --master-addr 127.0.0.1 \
+        --master-port P bench.py --gpus N ...
+
+One step = one encryption of the whole message (every row of SURVEY.md §8(a): per-block
+key schedule, Steps 1-3 with n_it RK4 steps per character, sentinel tag, tag combine)
+by all ranks, each rank owning a contiguous block range.
+
+Default workload C4 (BASELINE.json configs[3], which is the config quoted at 1/2/4/8
+B200 and fits one GPU): a 1 GiB synthetic message, FAST mode, n_it = 100, B = 1024,
+1,048,576 blocks, block-sharded over N ranks (fixed total work: strong scaling).
+
+Prints ONE JSON line (rank 0). value = whole-job encrypt MB/s (10^6 B/s) from device
+time (CUDA events on the launching stream, max over ranks); e2e = the same through the
+host-buffer C-ABI call with H2D/D2H inside the timed region; roofline = the chain
+kernel's FP64 DADD/DMUL rate against the B200 FP64 pipe; cpu_baseline =
+the CPU oracle on a bounded sample on this host's cores (rank 0, N = 1 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "encrypt/decrypt MB/s at 1/2/4/8 B200; FP64-pipe % of peak; bit-exact vs oracle"
+SMS = 148
+FP64_LANES_PER_SM = 64
+L2_BYTES = 126 * 2 ** 20
+OPS_PER_RK4_STEP = 75   # 43 DADD + 32 DMUL (SASS-verified, tools/sass_stats.py)
+OPS_PER_CHAR_EXTRA = 7  # 3 DMUL quantise + 1 DADD Theta + 3 DADD a'
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=int(os.environ.get("WORLD_SIZE", "1")))
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=["c4", "c3"], default="c4")
+    ap.add_argument("--n-it", type=int, default=100)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU time of the oracle sample")
+    return ap.parse_args()
+
+
+def workload(name: str):
+    if name == "c3":
+        return "C3: 64 MiB message, FAST, B=1024, on 1 B200", 64 << 20
+    return "C4: 1 GiB message, FAST, B=1024, block-sharded over N B200", 1 << 30
+
+
+def fp64_ops(n: int, B: int, b0: int, b1: int, n_it: int) -> int:
+    """Algorithmic FP64 ops (DADD+DMUL, no FMA) of blocks [b0,b1): each block advances
+    len_b + 15 characters (the last sentinel character is not advanced, Q20)."""
+    full = max(0, min(b1, n // B) - b0)
+    chars = full * (B + 15)
+    for b in range(max(b0, n // B), b1):
+        chars += (min(n, (b + 1) * B) - b * B) + 15
+    return chars * (OPS_PER_RK4_STEP * n_it + OPS_PER_CHAR_EXTRA)
+
+
+def cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# ---------------------------------------------------------------- clocks during the timed region
+class ClockSampler:
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap", "power.draw"]
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+
+    def __init__(self, gpu_id: str):
+        self.gpu_id, self.proc, self.path = gpu_id, None, None
+
+    def __enter__(self):
+        import tempfile
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", self.gpu_id, "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait(timeout=10)
+
+    def summary(self):
+        rows = []
+        try:
+            for ln in open(self.path):
+                parts = [p.strip() for p in ln.split(",")]
+                if len(parts) == len(self.FIELDS):
+                    rows.append(parts)
+        except OSError:
+            pass
+        finally:
+            if self.path and os.path.exists(self.path):
+                os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        sm = [num(r[0]) for r in rows if num(r[0])]
+        reasons = sorted({self.NAMES[i] for r in rows for i in range(4) if r[2 + i].lower().startswith("active")})
+        pw = [num(r[6]) for r in rows if num(r[6])]
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": num(rows[0][1]),
+                "reasons": reasons, "samples": len(rows), "power_w_max": max(pw) if pw else None}
+
+
+# ---------------------------------------------------------------- reference arm: the CPU oracle
+def run_reference(a):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    from paper_1201_3114_b200 import inputs
+    name, n = workload(a.workload)
+    B = 1024
+    pw = inputs.password()
+    prm = oracle.params(mode=oracle.FAST, n_it=a.n_it, block_size=B)
+    threads = cores()
+    # calibrate: blocks per step so that warmup + steps take ~2-3 minutes in total
+    probe = max(threads, 8)
+    msg = inputs.message(probe * B)
+    t0 = time.perf_counter()
+    oracle.encrypt(pw, msg, prm, b0=0, b1=probe, threads=threads)
+    per_block = (time.perf_counter() - t0) / probe
+    budget = 150.0 / max(1, a.steps + a.warmup)
+    S = int(max(threads, min(budget / per_block, (n // B))))
+    msg = inputs.message(S * B)
+    times = []
+    for i in range(a.warmup + a.steps):
+        t0 = time.perf_counter()
+        oracle.encrypt(pw, msg, prm, b0=0, b1=S, threads=threads)
+        dt = time.perf_counter() - t0
+        if i >= a.warmup:
+            times.append(dt)
+    sec = sum(times) / len(times)
+    mbps = S * B / sec / 1e6
+    sample = f"first {S} of the {n // B} blocks of the {name.split(':')[0]} message per step (n_it={a.n_it})"
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": round(mbps, 4), "unit": "MB/s", "n_gpus": a.gpus,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(sec * 1e3, 3), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (SplitMix64, DESIGN.md §6)",
+        "config": {"workload": name, "message_bytes": n, "block_size": B, "n_it": a.n_it, "mode": "FAST",
+                   "parallelism": f"cpu threads {threads}"},
+        "cpu_baseline": {"value": round(mbps, 4), "unit": "MB/s", "cores": threads, "kind": "oracle",
+                         "sample": sample, "cpu": cpu_model()},
+        "e2e": {"value": round(mbps, 4), "unit": "MB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def cpu_baseline(pw, n_it, B, n, target_s):
+    import oracle
+    from paper_1201_3114_b200 import inputs
+    prm = oracle.params(mode=oracle.FAST, n_it=n_it, block_size=B)
+    threads = cores()
+    probe = max(threads, 8)
+    msg = inputs.message(probe * B)
+    t0 = time.perf_counter()
+    oracle.encrypt(pw, msg, prm, b0=0, b1=probe, threads=threads)
+    per_block = (time.perf_counter() - t0) / probe
+    S = int(max(probe, min(target_s / per_block, n // B)))
+    msg = inputs.message(S * B)
+    t0 = time.perf_counter()
+    oracle.encrypt(pw, msg, prm, b0=0, b1=S, threads=threads)
+    sec = time.perf_counter() - t0
+    return {"value": round(S * B / sec / 1e6, 4), "unit": "MB/s", "cores": threads, "kind": "oracle",
+            "sample": f"blocks [0,{S}) of the same message ({S * B} bytes), all {threads} threads, "
+                      f"{sec:.1f} s", "cpu": cpu_model()}
+
+
+# ---------------------------------------------------------------- our arm
+def main():
+    a = parse()
+    if a.impl == "reference":
+        return run_reference(a)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1201_3114_b200 import dist as D
+    from paper_1201_3114_b200 import inputs
+    from paper_1201_3114_b200 import lorenz as L
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    name, n = workload(a.workload)
+    B = 1024
+    pw = inputs.password()
+    key = L.lorenz_keysetup(pw, mode=L.FAST, n_it=a.n_it, block_size=B)
+    nb = key.num_blocks(n)
+    b0, b1 = D.block_range(nb, rank, world)
+    sl = D.slice_of(n, B, b0, b1)
+    msg = inputs.message(sl.pt_bytes, start=sl.pt_off)
+    pt = torch.from_numpy(msg).to(dev)
+    ct = torch.empty(sl.ct_bytes, dtype=torch.uint8, device=dev)
+    back = torch.empty(sl.pt_bytes, dtype=torch.uint8, device=dev)
+    flush = torch.empty(2 * L2_BYTES, dtype=torch.uint8, device=dev)
+    eng = D.CudaEngine(key, n, dev)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def step_encrypt():
+        tag = eng.encrypt(b0, b1, pt, ct)
+        return D.xor_combine(tag) if world > 1 else tag
+
+    def step_decrypt():
+        eng.decrypt(b0, b1, ct, back)
+        return D.min_combine(eng.first_bad()) if world > 1 else eng.first_bad()
+
+    def timed(fn, K):
+        """K steps; L2 flushed (write > L2) between steps, outside the events."""
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+        barrier()
+        for s, e in ev:
+            flush.fill_(1)
+            s.record(stream)
+            fn()
+            e.record(stream)
+        barrier()
+        return [s.elapsed_time(e) for s, e in ev]
+
+    for _ in range(a.warmup):
+        step_encrypt()
+    barrier()
+    gpu_uuid = str(torch.cuda.get_device_properties(dev).uuid)
+    gpu_id = gpu_uuid if gpu_uuid.startswith("GPU-") else "GPU-" + gpu_uuid
+    with ClockSampler(gpu_id) as clk:
+        enc_ms = timed(step_encrypt, a.steps)
+    clocks = clk.summary()
+    tag = step_encrypt().cpu().numpy().tobytes()
+
+    for _ in range(min(a.warmup, 1)):
+        step_decrypt()
+    dec_ms = timed(step_decrypt, a.steps)
+    fb = int(step_decrypt().item())
+    ok = fb == D.NO_BAD and torch.equal(back, pt)
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    enc_sum = max_over_ranks(sum(enc_ms))
+    dec_sum = max_over_ranks(sum(dec_ms))
+    oks = max_over_ranks(0.0 if ok else 1.0) == 0.0
+    ms_step = enc_sum / a.steps
+    value = n / (ms_step / 1e3) / 1e6
+    dec_value = n / (dec_sum / a.steps / 1e3) / 1e6
+
+    # roofline: the chain kernel's algorithmic FP64 ops per launch / its event time (this rank)
+    ops = fp64_ops(n, B, b0, b1, a.n_it)
+    kern_s = statistics.mean(enc_ms) / 1e3
+    achieved = ops / kern_s / 1e12
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    peak = SMS * FP64_LANES_PER_SM * sm_max * 1e6 / 1e12
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_chain_kernel.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get("dram_bytes_per_launch_c4_rank_of", {}).get(str(world))
+        except (ValueError, OSError):
+            traffic = None
+
+    # e2e through the host-buffer C-ABI call (pinned host slices)
+    e2e = None
+    if not a.no_e2e:
+        pt_h = torch.from_numpy(msg).pin_memory()
+        ct_h = torch.empty(sl.ct_bytes, dtype=torch.uint8).pin_memory()
+        t_dev = torch.empty(16, dtype=torch.uint8, device=dev)
+        L.lorenz_encrypt_host(key, n, b0, b1, pt_h, ct_h)  # warm the pool and streams
+        times = []
+        for _ in range(a.steps):
+            barrier()
+            t0 = time.perf_counter()
+            t = L.lorenz_encrypt_host(key, n, b0, b1, pt_h, ct_h)
+            if world > 1:
+                t_dev.copy_(torch.frombuffer(bytearray(t), dtype=torch.uint8))
+                D.xor_combine(t_dev).cpu()
+            times.append(time.perf_counter() - t0)
+        e2e_s = max_over_ranks(statistics.mean(times))
+        e2e = {"value": round(n / e2e_s / 1e6, 3), "unit": "MB/s", "h2d_bytes_per_step": sl.pt_bytes,
+               "d2h_bytes_per_step": sl.ct_bytes + 16, "api": "lorenz_encrypt_host (pinned host buffers)",
+               "ms_per_step": round(e2e_s * 1e3, 3), "matches_device_ct": bool(torch.equal(ct_h.to(dev), ct))}
+
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        cpu = cpu_baseline(pw, a.n_it, B, n, a.cpu_seconds)
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": round(value, 3), "unit": "MB/s", "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (SplitMix64 message, printable password)",
+            "config": {"workload": name, "message_bytes": n, "blocks": nb, "block_size": B, "n_it": a.n_it,
+                       "mode": "FAST", "integrator": "RK4", "dt": 0.01, "parallelism": f"blocks{world}",
+                       "l2": "flushed between timed steps (2x126 MB write) and inputs > L2"},
+            "decrypt": {"value": round(dec_value, 3), "unit": "MB/s", "ms_per_step": round(dec_sum / a.steps, 3)},
+            "roofline": {"bound": "alu", "achieved": round(achieved, 4), "peak": round(peak, 4), "unit": "TFLOP/s",
+                         "frac": round(achieved / peak, 4), "traffic": traffic,
+                         "kernel": "lz::lorenz_chain_kernel<ENC,RK4>",
+                         "ops_per_launch": ops, "peak_basis": "148 SM x 64 FP64 lanes x sm_max_mhz (DESIGN.md §4)",
+                         "hbm_gbs": round((sl.pt_bytes + sl.ct_bytes) / kern_s / 1e9, 3)},
+            "fp64_pipe_pct": round(100 * achieved / peak, 2),
+            "validated": {"round_trip": oks, "tag_xor": tag.hex()},
+            "e2e": e2e,
+            "gpu_launches": 2 * a.steps,
+            "clocks": clocks,
+        }
+        if cpu:
+            out["cpu_baseline"] = cpu
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,174 @@
+/* lorenz.h — C ABI of the B200-native hot path of the parallel Lorenz-attractor
+ * cipher of Marco, Martinez & Bruno, arXiv 1201.3114 ("Fast, parallel and secure
+ * cryptography algorithm using Lorenz's attractor"): the per-block chaotic
+ * operation mode.
+ *
+ * Library: paper_1201_3114_b200/csrc/liblorenz.so (CUDA, sm_100a). Python binding:
+ * paper_1201_3114_b200/lorenz.py (same names, argument marshalling only).
+ *
+ * Citations: "P:n" = PAPER.md line n (section, equation); "S:n" = SPEC.md line n;
+ * "Qn" = reading n of DESIGN.md §3. The operation every entry point computes is
+ * defined in DESIGN.md §2; in short, for each block b of a message:
+ *   key schedule  (§3.1, Eqs.2-7)   password -> a, a', lambda, r0, mu, alpha, k, Omega
+ *   per character (§3.2, Steps 1-3) C_i = [P_i + R(alpha1,Omega1) + R(alpha2,Omega2)] mod 2^8
+ *                                              (Eqs.8-9); Theta = P_i/10^{3+Omega3} added to r[mu3];
+ *                                              n_it fixed-step RK4 steps of the Lorenz system (Eq.1, Q1-Q3);
+ *                                              mu, alpha, Omega update; r += a'
+ *   integrity     (§2)              16-byte sentinel "LORENZCHAOS-MAC1" appended to every
+ *                                              block's plaintext; its ciphertext is the block tag (Q15)
+ *   parallel mode (§5)              FAST: fixed B-byte blocks, block b keyed by
+ *                                              SHA-256(pw || BE32 b)[0:18] (Q16); STRONG: one stream.
+ *
+ * Conventions shared by every call
+ *   - All arithmetic is IEEE binary64 round-to-nearest with no fused multiply-add, in
+ *     the operation order of DESIGN.md §2, so results are bit-identical on every
+ *     conforming implementation (and to the CPU oracle in oracle/).
+ *   - Device pointers are plain CUDA device addresses (e.g. torch.Tensor.data_ptr()),
+ *     16-byte aligned; the caller owns every buffer. `cuda_stream` is a cudaStream_t
+ *     (NULL = legacy default stream). Calls without the _async suffix enqueue their
+ *     work on that stream and synchronise it before returning.
+ *   - Errors are returned, never raised: no abort/exit. Argument errors are reported
+ *     before anything is enqueued. After LORENZ_E_CUDA, lorenz_last_error() holds the
+ *     CUDA error text of the calling thread.
+ *   - Layout: block b of the message covers plaintext bytes [b*B, min(n,(b+1)*B)) and
+ *     ciphertext bytes [b*(B+16), b*(B+16) + len_b + 16): its body then its 16-byte
+ *     tag (Q21). STRONG is a single block with B = n.
+ */
+#ifndef LORENZ_H
+#define LORENZ_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LORENZ_TAG_BYTES 16
+#define LORENZ_KEY_BYTES 384
+#define LORENZ_ABI_VERSION 1
+
+typedef enum {
+  LORENZ_OK = 0,
+  LORENZ_E_INTEGRITY = 1,  /* a recovered sentinel differs; mirrors SPEC exit code 1 */
+  LORENZ_E_ARG = 2,        /* NULL / misaligned pointer, bad range or params                           */
+  LORENZ_E_PASSWORD = 3,   /* password shorter than 3 bytes (Q17)                                 */
+  LORENZ_E_LENGTH = 4,     /* ciphertext length inconsistent with the block size                 */
+  LORENZ_E_DIVERGENCE = 5, /* guard: non-finite or |x|,|y|>100, z outside [-50,150] (Q18)                */
+  LORENZ_E_CUDA = 6        /* a CUDA runtime error; see lorenz_last_error()                              */
+} lorenz_status;
+
+typedef enum { LORENZ_STRONG = 0, LORENZ_FAST = 1 } lorenz_mode;           /* P:446-448 §5 */
+typedef enum { LORENZ_RK4 = 0, LORENZ_EULER = 1 } lorenz_integrator;       /* Q1 */
+
+typedef struct {
+  uint32_t mode;       /* lorenz_mode                                                             */
+  uint32_t n_it;       /* RK4 steps per character; 0 -> 3000 (STRONG) / 100 (FAST)      */
+  uint32_t dt_code;    /* step h: 0 -> 0.01, 1 -> 0.005, 2 -> 0.02, 3 -> 0.027 (0 < h <= 0.027) */
+  uint32_t block_size; /* FAST block size B: >= 1024 and a multiple of 16; 0 -> 1024. STRONG: ignored */
+  uint32_t integrator; /* lorenz_integrator; LORENZ_EULER is the paper's own discretisation  */
+} lorenz_params;
+
+/* Key: POD, caller-owned, trivially copyable, no heap. Holds the params, the exact
+ * binary64 bit patterns of sigma, rho, beta, h, h/2, h/6, and the password:
+ * STRONG: the normalised password (3..23 bytes; longer ones are replaced by
+ * SHA-256(pw)[0:18]); FAST: the SHA-256 midstate of the raw password so the
+ * device finishes SHA-256(pw || BE32 b) per block. */
+typedef struct { uint8_t opaque[LORENZ_KEY_BYTES]; } lorenz_key;
+
+/* Device-side result slot for the _async calls (caller-allocated device memory,
+ * 32 bytes, 16-byte aligned; initialise with lorenz_result_init_async). */
+typedef struct {
+  uint8_t tag_xor[16];       /* XOR of the tags of the processed blocks (Q15)              */
+  uint64_t first_bad;        /* min failing global block index, UINT64_MAX if none         */
+  uint32_t status;           /* OR of per-lane flags: 1 = integrity, 4 = divergence         */
+  uint32_t reserved;
+} lorenz_result;
+
+/* ---- host-only helpers (no device work) ---- */
+
+/* Derive a key. pw: pw_len bytes (host). p: NULL -> FAST defaults.
+ * Errors: LORENZ_E_PASSWORD if pw_len < 3; LORENZ_E_ARG for bad params/NULL.
+ * Deterministic: same bytes and params -> bit-identical key. */
+lorenz_status lorenz_keysetup(const uint8_t* pw, size_t pw_len, const lorenz_params* p,
+                              lorenz_key* out);
+/* Effective params stored in a key (defaults filled in). */
+lorenz_status lorenz_key_params(const lorenz_key* k, lorenz_params* out);
+/* FAST: max(1, ceil(n/B)); STRONG: 1. 0 for an invalid key. */
+uint64_t lorenz_num_blocks(const lorenz_key* k, uint64_t n);
+/* n + 16 * lorenz_num_blocks(k, n). */
+uint64_t lorenz_ct_len(const lorenz_key* k, uint64_t n);
+/* Inverse of lorenz_ct_len; LORENZ_E_LENGTH if no n maps to ct_len. */
+lorenz_status lorenz_pt_len(const lorenz_key* k, uint64_t ct_len, uint64_t* n_out);
+const char* lorenz_status_string(lorenz_status s);
+const char* lorenz_last_error(void);
+int lorenz_abi_version(void);
+
+/* ---- device calls: global blocks [b0, b1) of a message of total plaintext length n ----
+ * pt / ct are DEVICE pointers to the start of the SLICE: pt = message + b0*B,
+ * ct = ciphertext + b0*(B+16) (so a rank can hold only its own slice). The slice
+ * holds min(n, b1*B) - b0*B plaintext bytes and that + 16*(b1-b0) ciphertext bytes.
+ * pt and ct must not overlap. b0 == b1 is a no-op (tag_xor = 0). */
+
+/* C = E_pi(P) (Eq.9, Steps 1-3). tag_xor (host, 16 B, nullable) receives the
+ * XOR of the tags of blocks [b0,b1). */
+lorenz_status lorenz_encrypt(const lorenz_key* k, uint64_t n, uint64_t b0, uint64_t b1,
+                             const uint8_t* pt, uint8_t* ct, uint8_t tag_xor[16],
+                             void* cuda_stream);
+
+/* P = D_pi(C) (Eq.10; the chain advances with the recovered byte).
+ * first_bad_block (host, nullable): min failing global block, -1 if none.
+ * block_ok (DEVICE, nullable, b1-b0 bytes): per-block verdict 1/0. With block_ok,
+ * only failing blocks' plaintext is zero-filled; without it, the whole slice is
+ * zero-filled on failure (so unauthenticated plaintext is never released).
+ * Returns LORENZ_E_INTEGRITY if any block fails. */
+lorenz_status lorenz_decrypt(const lorenz_key* k, uint64_t n, uint64_t b0, uint64_t b1,
+                             const uint8_t* ct, uint8_t* pt, int64_t* first_bad_block,
+                             uint8_t* block_ok, void* cuda_stream);
+
+/* Decrypt without writing plaintext: integrity check only.
+ * tag_xor (host, nullable): XOR of the ciphertext's block tags. */
+lorenz_status lorenz_verify(const lorenz_key* k, uint64_t n, uint64_t b0, uint64_t b1,
+                            const uint8_t* ct, int64_t* first_bad_block, uint8_t tag_xor[16],
+                            void* cuda_stream);
+
+/* ---- asynchronous forms: enqueue and return; results accumulate into `res`
+ * (device, see lorenz_result). Safe inside CUDA graph capture. ---- */
+lorenz_status lorenz_result_init_async(lorenz_result* res, void* cuda_stream);
+lorenz_status lorenz_encrypt_async(const lorenz_key* k, uint64_t n, uint64_t b0, uint64_t b1,
+                                   const uint8_t* pt, uint8_t* ct, lorenz_result* res,
+                                   void* cuda_stream);
+lorenz_status lorenz_decrypt_async(const lorenz_key* k, uint64_t n, uint64_t b0, uint64_t b1,
+                                   const uint8_t* ct, uint8_t* pt, uint8_t* block_ok,
+                                   lorenz_result* res, void* cuda_stream);
+lorenz_status lorenz_verify_async(const lorenz_key* k, uint64_t n, uint64_t b0, uint64_t b1,
+                                  const uint8_t* ct, lorenz_result* res, void* cuda_stream);
+
+/* ---- batch (C5 sweeps): S independent messages of equal length n, one key each
+ * (all keys must share mode/n_it/dt/B/integrator, else LORENZ_E_ARG). keys: HOST
+ * array of S keys. Message s is at pts + s*n, its ciphertext at cts + s*ct_len(n),
+ * its tag XOR at tags + 16*s (all DEVICE). One launch, lane = (message, block). */
+lorenz_status lorenz_encrypt_batch(const lorenz_key* keys, uint32_t S, uint64_t n,
+                                   const uint8_t* pts, uint8_t* cts, uint8_t* tags,
+                                   void* cuda_stream);
+
+/* ---- end to end from HOST buffers (the user-facing call of a file encryptor):
+ * blocks [b0,b1) of an n-byte message; pt_host / ct_host are HOST pointers to the
+ * slice starts (same slice convention as the device calls; [0, num_blocks) is the
+ * whole message). Host->device copies, kernels and device->host copies are
+ * pipelined over `n_chunks` block-aligned chunks on internal streams (0 ->
+ * automatic) on the current device. Pinned host memory gives overlapped copies;
+ * pageable memory works but copies synchronously. Allocates its own device buffers
+ * from the stream-ordered pool (kept cached between calls). Synchronous.
+ * decrypt: on LORENZ_E_INTEGRITY the whole host plaintext slice is zero-filled. */
+lorenz_status lorenz_encrypt_host(const lorenz_key* k, uint64_t n, uint64_t b0, uint64_t b1,
+                                  const uint8_t* pt_host, uint8_t* ct_host, uint8_t tag_xor[16],
+                                  uint32_t n_chunks);
+lorenz_status lorenz_decrypt_host(const lorenz_key* k, uint64_t n, uint64_t b0, uint64_t b1,
+                                  const uint8_t* ct_host, uint8_t* pt_host,
+                                  int64_t* first_bad_block, uint32_t n_chunks);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LORENZ_H */

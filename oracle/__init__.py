@@ -98,6 +98,8 @@ def lib():
         L.lorenz_ref_pt_len.argtypes = [C.POINTER(Params), C.c_uint64, u64p]
         L.lorenz_ref_encrypt.argtypes = [C.c_char_p, C.c_size_t, C.POINTER(Params), C.c_uint64, C.c_uint64,
                                          C.c_uint64, C.c_void_p, C.c_void_p, u8p, C.c_int]
+        L.lorenz_ref_encrypt_block.argtypes = [C.c_char_p, C.c_size_t, C.POINTER(Params), C.c_uint64,
+                                               C.c_uint64, C.c_void_p, C.c_void_p]
         L.lorenz_ref_decrypt.argtypes = [C.c_char_p, C.c_size_t, C.POINTER(Params), C.c_uint64, C.c_uint64,
                                          C.c_uint64, C.c_void_p, C.c_void_p, C.POINTER(C.c_int64),
                                          C.c_void_p, C.c_int]
@@ -291,6 +293,17 @@ def encrypt(pw: bytes, pt, prm: Params, b0=0, b1=None, threads=0):
     if st:
         raise OracleError(st)
     return ct, bytes(tag)
+
+
+def encrypt_block(pw: bytes, n: int, b: int, blk_pt, prm: Params) -> np.ndarray:
+    """Ciphertext (body + tag) of global block b of an n-byte message, from its bytes."""
+    pa = _buf(blk_pt)
+    ct = np.zeros(len(pa) + 16, dtype=np.uint8)
+    st = lib().lorenz_ref_encrypt_block(pw, len(pw), C.byref(prm), n, b, pa.ctypes.data if len(pa) else None,
+                                        ct.ctypes.data)
+    if st:
+        raise OracleError(st)
+    return ct
 
 
 def decrypt(pw: bytes, ct, prm: Params, b0=0, b1=None, threads=0, per_block=False):

@@ -566,6 +566,24 @@ int lorenz_ref_encrypt(const uint8_t* pw, size_t pw_len, const lref_params* prm_
   return LREF_OK;
 }
 
+/* One global block b of a message of length n, from that block's own bytes:
+ * blk_pt = the block's plaintext (len_b bytes), blk_ct receives len_b + 16 bytes. */
+int lorenz_ref_encrypt_block(const uint8_t* pw, size_t pw_len, const lref_params* prm_in, uint64_t n,
+                             uint64_t b, const uint8_t* blk_pt, uint8_t* blk_ct) {
+  lref_params prm;
+  fill_defaults(prm_in, &prm);
+  if (check_params(&prm)) return LREF_E_ARG;
+  if (pw_len < 3) return LREF_E_PASSWORD;
+  if (b >= lorenz_ref_num_blocks(&prm, n)) return LREF_E_ARG;
+  uint64_t B = prm.mode == LREF_FAST ? prm.block_size : n;
+  uint64_t start = prm.mode == LREF_FAST ? b * B : 0;
+  uint64_t len = n - start < B ? n - start : B;
+  lref_km km;
+  int st = block_km(pw, pw_len, &prm, b, &km);
+  if (st) return st;
+  return lorenz_ref_encrypt_stream(&km, &prm, blk_pt, (size_t)len, blk_ct, NULL);
+}
+
 int lorenz_ref_decrypt(const uint8_t* pw, size_t pw_len, const lref_params* prm_in, uint64_t n,
                        uint64_t b0, uint64_t b1, const uint8_t* ct, uint8_t* pt,
                        int64_t* first_bad, uint8_t* block_ok, int threads) {

@@ -99,6 +99,9 @@ int lorenz_ref_pt_len(const lref_params* prm, uint64_t ct_len, uint64_t* n_out);
 int lorenz_ref_encrypt(const uint8_t* pw, size_t pw_len, const lref_params* prm, uint64_t n,
                        uint64_t b0, uint64_t b1, const uint8_t* pt, uint8_t* ct,
                        uint8_t tag_xor[16], int threads);
+/* One global block b of a message of length n, from that block's own bytes. */
+int lorenz_ref_encrypt_block(const uint8_t* pw, size_t pw_len, const lref_params* prm, uint64_t n,
+                             uint64_t b, const uint8_t* blk_pt, uint8_t* blk_ct);
 /* block_ok (nullable): per-block verdict for [b0,b1); when given, only failing
  * blocks are zero-filled, otherwise the whole range is zero-filled on failure. */
 int lorenz_ref_decrypt(const uint8_t* pw, size_t pw_len, const lref_params* prm, uint64_t n,

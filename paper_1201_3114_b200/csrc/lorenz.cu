@@ -1,0 +1,583 @@
+// lorenz.cu — host side of liblorenz.so: the C ABI of include/lorenz.h.
+//
+// Validates arguments, builds the per-launch constant block and password material
+// from a lorenz_key, launches the sm_100a kernels of lorenz_device.cuh on the
+// caller's stream, and reads back tag / verdict. No CPU fallback: every byte of
+// ciphertext is produced on the GPU.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/lorenz.h"
+#include "lorenz_device.cuh"
+#include "sha256.cuh"
+
+namespace {
+
+constexpr uint32_t kMagic = 0x314B5A4Cu;  // "LZK1"
+
+struct KeyImpl {
+  uint32_t magic;
+  uint32_t abi;
+  lorenz_params prm;        // defaults filled in
+  uint32_t pw_len;          // STRONG: normalised password length (3..23)
+  double sigma, rho, beta;
+  double h, h2, h6;         // step (P:187 range), h*0.5, h/6.0 — rounded once, here
+  uint8_t pw[24];           // STRONG: normalised password
+  uint32_t mid[8];          // FAST: SHA-256 midstate of the raw password's full blocks
+  uint64_t raw_len;         // FAST: raw password length
+  uint32_t tail_len;        // FAST: raw_len mod 64
+  uint8_t tail[64];         // FAST: the raw password's last partial block
+};
+static_assert(sizeof(KeyImpl) <= LORENZ_KEY_BYTES, "key layout exceeds the ABI size");
+
+thread_local std::string g_err;
+
+const KeyImpl* impl(const lorenz_key* k) {
+  if (!k) return nullptr;
+  const KeyImpl* K = reinterpret_cast<const KeyImpl*>(k->opaque);
+  return (K->magic == kMagic && K->abi == LORENZ_ABI_VERSION) ? K : nullptr;
+}
+
+bool cuda_ok(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return true;
+  g_err = std::string(what) + ": " + cudaGetErrorString(e);
+  return false;
+}
+
+double dt_of(uint32_t code) {
+  switch (code) {
+    case 0: return 0.01;
+    case 1: return 0.005;
+    case 2: return 0.02;
+    default: return 0.027;
+  }
+}
+
+uint64_t nblocks(const KeyImpl* K, uint64_t n) {
+  if (K->prm.mode == LORENZ_STRONG) return 1;
+  const uint64_t B = K->prm.block_size;
+  const uint64_t nb = (n + B - 1) / B;
+  return nb ? nb : 1;
+}
+
+uint64_t block_B(const KeyImpl* K, uint64_t n) {
+  return K->prm.mode == LORENZ_FAST ? K->prm.block_size : n;
+}
+
+// plaintext / ciphertext byte extents of blocks [b0,b1)
+void slice_bytes(const KeyImpl* K, uint64_t n, uint64_t b0, uint64_t b1, uint64_t* pt_bytes,
+                 uint64_t* ct_bytes) {
+  const uint64_t B = block_B(K, n);
+  const uint64_t hi = (K->prm.mode == LORENZ_FAST) ? ((b1 * B < n) ? b1 * B : n) : n;
+  const uint64_t lo = (K->prm.mode == LORENZ_FAST) ? b0 * B : 0;
+  *pt_bytes = hi - lo;
+  *ct_bytes = hi - lo + 16 * (b1 - b0);
+}
+
+void put_words_be(const uint8_t* bytes, int nwords, uint32_t* w) {
+  for (int i = 0; i < nwords; ++i)
+    w[i] = (uint32_t)bytes[4 * i] << 24 | (uint32_t)bytes[4 * i + 1] << 16 |
+           (uint32_t)bytes[4 * i + 2] << 8 | bytes[4 * i + 3];
+}
+
+lz::DevKey make_devkey(const KeyImpl* K) {
+  lz::DevKey d;
+  std::memset(&d, 0, sizeof d);
+  if (K->prm.mode == LORENZ_FAST) {
+    for (int i = 0; i < 8; ++i) d.mid[i] = K->mid[i];
+    uint8_t fin[128] = {0};
+    const uint32_t t = K->tail_len;
+    std::memcpy(fin, K->tail, t);
+    // fin[t..t+3] = BE32(b), filled per lane on the device
+    fin[t + 4] = 0x80;
+    const uint32_t nbk = (t + 4 + 1 + 8 <= 64) ? 1 : 2;
+    const uint64_t bits = (K->raw_len + 4) * 8;
+    for (int i = 0; i < 8; ++i) fin[64 * nbk - 1 - i] = (uint8_t)(bits >> (8 * i));
+    put_words_be(fin, 32, d.fin);
+    d.fin_blocks = nbk;
+    d.b_off = t;
+  } else {
+    uint8_t pw[24] = {0};
+    std::memcpy(pw, K->pw, K->pw_len);
+    put_words_be(pw, 6, d.pw);
+    d.pw_len = K->pw_len;
+  }
+  return d;
+}
+
+lz::DevConst make_const(const KeyImpl* K, uint64_t n, uint64_t b0, uint64_t lanes) {
+  lz::DevConst C;
+  std::memset(&C, 0, sizeof C);
+  C.sigma = K->sigma; C.rho = K->rho; C.beta = K->beta;
+  C.h = K->h; C.h2 = K->h2; C.h6 = K->h6;
+  C.n = n;
+  C.B = block_B(K, n);
+  C.b0 = b0;
+  C.lanes = lanes;
+  C.nb = nblocks(K, n);
+  C.n_it = K->prm.n_it;
+  C.fast = K->prm.mode == LORENZ_FAST;
+  return C;
+}
+
+template <int OP>
+cudaError_t launch_chain(const lz::DevConst& C, const lz::DevKey& K, const lz::DevKey* Kb,
+                         uint32_t integrator, const uint8_t* in, uint8_t* out, lorenz_result* res,
+                         uint8_t* tags, uint8_t* block_ok, cudaStream_t st) {
+  const uint64_t grid = (C.lanes + lz::kCta - 1) / lz::kCta;
+  if (grid == 0) return cudaSuccess;
+  if (integrator == LORENZ_EULER)
+    lz::lorenz_chain_kernel<OP, LORENZ_EULER><<<(unsigned)grid, lz::kCta, 0, st>>>(C, K, Kb, in, out, res, tags, block_ok);
+  else
+    lz::lorenz_chain_kernel<OP, LORENZ_RK4><<<(unsigned)grid, lz::kCta, 0, st>>>(C, K, Kb, in, out, res, tags, block_ok);
+  return cudaGetLastError();
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+bool overlap(const void* a, uint64_t na, const void* b, uint64_t nb) {
+  if (!na || !nb) return false;
+  const uintptr_t x = reinterpret_cast<uintptr_t>(a), y = reinterpret_cast<uintptr_t>(b);
+  return x < y + nb && y < x + na;
+}
+
+// Shared validation of the device block-range calls.
+lorenz_status check_range(const KeyImpl* K, uint64_t n, uint64_t b0, uint64_t b1, const void* in,
+                          uint64_t in_bytes, const void* out, uint64_t out_bytes) {
+  if (!K) return LORENZ_E_ARG;
+  const uint64_t nb = nblocks(K, n);
+  if (b0 > b1 || b1 > nb) return LORENZ_E_ARG;
+  if (K->prm.mode == LORENZ_FAST && nb > (1ULL << 32)) return LORENZ_E_ARG;  // BE32 block index
+  if (in_bytes && (!in || !aligned16(in))) return LORENZ_E_ARG;
+  if (out_bytes && (!out || !aligned16(out))) return LORENZ_E_ARG;
+  if (overlap(in, in_bytes, out, out_bytes)) return LORENZ_E_ARG;
+  return LORENZ_OK;
+}
+
+lorenz_status finish_sync(lorenz_result* d_res, cudaStream_t st, lorenz_result* h_res) {
+  if (!cuda_ok(cudaMemcpyAsync(h_res, d_res, sizeof *h_res, cudaMemcpyDeviceToHost, st), "readback"))
+    return LORENZ_E_CUDA;
+  if (!cuda_ok(cudaFreeAsync(d_res, st), "cudaFreeAsync")) return LORENZ_E_CUDA;
+  if (!cuda_ok(cudaStreamSynchronize(st), "cudaStreamSynchronize")) return LORENZ_E_CUDA;
+  if (h_res->status & lz::ST_DIVERGENCE) return LORENZ_E_DIVERGENCE;
+  if (h_res->status & lz::ST_INTEGRITY) return LORENZ_E_INTEGRITY;
+  return LORENZ_OK;
+}
+
+lorenz_status alloc_result(lorenz_result** d_res, cudaStream_t st) {
+  if (!cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(d_res), sizeof(lorenz_result), st), "cudaMallocAsync"))
+    return LORENZ_E_CUDA;
+  lz::result_init_kernel<<<1, 32, 0, st>>>(*d_res);
+  return cuda_ok(cudaGetLastError(), "result_init") ? LORENZ_OK : LORENZ_E_CUDA;
+}
+
+}  // namespace
+
+// ======================================================================== C ABI
+extern "C" {
+
+int lorenz_abi_version(void) { return LORENZ_ABI_VERSION; }
+
+const char* lorenz_last_error(void) { return g_err.c_str(); }
+
+const char* lorenz_status_string(lorenz_status s) {
+  switch (s) {
+    case LORENZ_OK: return "ok";
+    case LORENZ_E_INTEGRITY: return "integrity check failed (a block's sentinel did not decrypt)";
+    case LORENZ_E_ARG: return "invalid argument";
+    case LORENZ_E_PASSWORD: return "password shorter than 3 bytes";
+    case LORENZ_E_LENGTH: return "ciphertext length inconsistent with the block size";
+    case LORENZ_E_DIVERGENCE: return "trajectory left the guard box";
+    case LORENZ_E_CUDA: return "CUDA runtime error";
+  }
+  return "unknown status";
+}
+
+lorenz_status lorenz_keysetup(const uint8_t* pw, size_t pw_len, const lorenz_params* p, lorenz_key* out) {
+  if (!out || (!pw && pw_len)) return LORENZ_E_ARG;
+  lorenz_params prm = p ? *p : lorenz_params{LORENZ_FAST, 0, 0, 0, LORENZ_RK4};
+  if (prm.mode > 1 || prm.dt_code > 3 || prm.integrator > 1) return LORENZ_E_ARG;
+  if (prm.n_it == 0) prm.n_it = prm.mode == LORENZ_FAST ? 100u : 3000u;
+  if (prm.mode == LORENZ_FAST) {
+    if (prm.block_size == 0) prm.block_size = 1024;
+    if (prm.block_size < 1024 || prm.block_size % 16) return LORENZ_E_ARG;
+  } else {
+    prm.block_size = 0;
+  }
+  if (pw_len < 3) return LORENZ_E_PASSWORD;
+  std::memset(out->opaque, 0, sizeof out->opaque);
+  KeyImpl* K = reinterpret_cast<KeyImpl*>(out->opaque);
+  K->magic = kMagic;
+  K->abi = LORENZ_ABI_VERSION;
+  K->prm = prm;
+  volatile double three = 3.0, six = 6.0;  // computed at run time, RN, like the oracle
+  K->sigma = 10.0;
+  K->rho = 28.0;
+  K->beta = 8.0 / three;
+  K->h = dt_of(prm.dt_code);
+  K->h2 = K->h * 0.5;
+  K->h6 = K->h / six;
+  if (prm.mode == LORENZ_STRONG) {
+    if (pw_len > 23) {  // longer passwords are replaced by SHA-256(pw)[0:18]
+      uint8_t d[32];
+      lz::sha256_host(pw, pw_len, d);
+      std::memcpy(K->pw, d, 18);
+      K->pw_len = 18;
+    } else {
+      std::memcpy(K->pw, pw, pw_len);
+      K->pw_len = (uint32_t)pw_len;
+    }
+  } else {
+    lz::Sha256State s;
+    s.init();
+    uint64_t off = 0;
+    uint32_t w[16];
+    for (; off + 64 <= pw_len; off += 64) {
+      put_words_be(pw + off, 16, w);
+      s.compress(w);
+    }
+    for (int i = 0; i < 8; ++i) K->mid[i] = s.h[i];
+    K->raw_len = pw_len;
+    K->tail_len = (uint32_t)(pw_len - off);
+    std::memcpy(K->tail, pw + off, K->tail_len);
+  }
+  return LORENZ_OK;
+}
+
+lorenz_status lorenz_key_params(const lorenz_key* k, lorenz_params* out) {
+  const KeyImpl* K = impl(k);
+  if (!K || !out) return LORENZ_E_ARG;
+  *out = K->prm;
+  return LORENZ_OK;
+}
+
+uint64_t lorenz_num_blocks(const lorenz_key* k, uint64_t n) {
+  const KeyImpl* K = impl(k);
+  return K ? nblocks(K, n) : 0;
+}
+
+uint64_t lorenz_ct_len(const lorenz_key* k, uint64_t n) {
+  const KeyImpl* K = impl(k);
+  return K ? n + 16 * nblocks(K, n) : 0;
+}
+
+lorenz_status lorenz_pt_len(const lorenz_key* k, uint64_t ct_len, uint64_t* n_out) {
+  const KeyImpl* K = impl(k);
+  if (!K || !n_out) return LORENZ_E_ARG;
+  if (ct_len < 16) return LORENZ_E_LENGTH;
+  if (K->prm.mode == LORENZ_STRONG) { *n_out = ct_len - 16; return LORENZ_OK; }
+  const uint64_t per = (uint64_t)K->prm.block_size + 16;
+  const uint64_t nb = (ct_len + per - 1) / per;
+  if (ct_len < 16 * nb) return LORENZ_E_LENGTH;
+  const uint64_t n = ct_len - 16 * nb;
+  if (nblocks(K, n) != nb) return LORENZ_E_LENGTH;
+  *n_out = n;
+  return LORENZ_OK;
+}
+
+lorenz_status lorenz_result_init_async(lorenz_result* res, void* stream) {
+  if (!res || !aligned16(res)) return LORENZ_E_ARG;
+  lz::result_init_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(res);
+  return cuda_ok(cudaGetLastError(), "result_init") ? LORENZ_OK : LORENZ_E_CUDA;
+}
+
+lorenz_status lorenz_encrypt_async(const lorenz_key* k, uint64_t n, uint64_t b0, uint64_t b1,
+                                   const uint8_t* pt, uint8_t* ct, lorenz_result* res, void* stream) {
+  const KeyImpl* K = impl(k);
+  if (!K || !res) return LORENZ_E_ARG;
+  uint64_t ptb = 0, ctb = 0;
+  if (b0 < b1) slice_bytes(K, n, b0, b1, &ptb, &ctb);
+  lorenz_status s = check_range(K, n, b0, b1, pt, ptb, ct, ctb);
+  if (s != LORENZ_OK || b0 == b1) return s;
+  const lz::DevConst C = make_const(K, n, b0, b1 - b0);
+  const lz::DevKey D = make_devkey(K);
+  return cuda_ok(launch_chain<lz::OP_ENC>(C, D, nullptr, K->prm.integrator, pt, ct, res, nullptr, nullptr,
+                                          (cudaStream_t)stream), "encrypt launch")
+             ? LORENZ_OK : LORENZ_E_CUDA;
+}
+
+lorenz_status lorenz_decrypt_async(const lorenz_key* k, uint64_t n, uint64_t b0, uint64_t b1,
+                                   const uint8_t* ct, uint8_t* pt, uint8_t* block_ok, lorenz_result* res,
+                                   void* stream) {
+  const KeyImpl* K = impl(k);
+  if (!K || !res) return LORENZ_E_ARG;
+  uint64_t ptb = 0, ctb = 0;
+  if (b0 < b1) slice_bytes(K, n, b0, b1, &ptb, &ctb);
+  lorenz_status s = check_range(K, n, b0, b1, ct, ctb, pt, ptb);
+  if (s != LORENZ_OK || b0 == b1) return s;
+  const lz::DevConst C = make_const(K, n, b0, b1 - b0);
+  const lz::DevKey D = make_devkey(K);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!cuda_ok(launch_chain<lz::OP_DEC>(C, D, nullptr, K->prm.integrator, ct, pt, res, nullptr, block_ok, st),
+               "decrypt launch"))
+    return LORENZ_E_CUDA;
+  if (!block_ok && ptb) {
+    lz::zero_if_failed_kernel<<<256, 256, 0, st>>>(res, pt, ptb);
+    if (!cuda_ok(cudaGetLastError(), "zero_if_failed")) return LORENZ_E_CUDA;
+  }
+  return LORENZ_OK;
+}
+
+lorenz_status lorenz_verify_async(const lorenz_key* k, uint64_t n, uint64_t b0, uint64_t b1, const uint8_t* ct,
+                                  lorenz_result* res, void* stream) {
+  const KeyImpl* K = impl(k);
+  if (!K || !res) return LORENZ_E_ARG;
+  uint64_t ptb = 0, ctb = 0;
+  if (b0 < b1) slice_bytes(K, n, b0, b1, &ptb, &ctb);
+  lorenz_status s = check_range(K, n, b0, b1, ct, ctb, nullptr, 0);
+  if (s != LORENZ_OK || b0 == b1) return s;
+  const lz::DevConst C = make_const(K, n, b0, b1 - b0);
+  const lz::DevKey D = make_devkey(K);
+  return cuda_ok(launch_chain<lz::OP_VERIFY>(C, D, nullptr, K->prm.integrator, ct, nullptr, res, nullptr,
+                                             nullptr, (cudaStream_t)stream), "verify launch")
+             ? LORENZ_OK : LORENZ_E_CUDA;
+}
+
+lorenz_status lorenz_encrypt(const lorenz_key* k, uint64_t n, uint64_t b0, uint64_t b1, const uint8_t* pt,
+                             uint8_t* ct, uint8_t tag_xor[16], void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const KeyImpl* K = impl(k);
+  if (!K) return LORENZ_E_ARG;
+  if (tag_xor) std::memset(tag_xor, 0, 16);
+  uint64_t ptb = 0, ctb = 0;
+  if (b0 < b1) slice_bytes(K, n, b0, b1, &ptb, &ctb);
+  lorenz_status s = check_range(K, n, b0, b1, pt, ptb, ct, ctb);
+  if (s != LORENZ_OK || b0 == b1) return s;
+  lorenz_result* d_res = nullptr;
+  if ((s = alloc_result(&d_res, st)) != LORENZ_OK) return s;
+  s = lorenz_encrypt_async(k, n, b0, b1, pt, ct, d_res, stream);
+  lorenz_result h;
+  lorenz_status f = finish_sync(d_res, st, &h);
+  if (s != LORENZ_OK) return s;
+  if (f == LORENZ_OK && tag_xor) std::memcpy(tag_xor, h.tag_xor, 16);
+  return f;
+}
+
+lorenz_status lorenz_decrypt(const lorenz_key* k, uint64_t n, uint64_t b0, uint64_t b1, const uint8_t* ct,
+                             uint8_t* pt, int64_t* first_bad_block, uint8_t* block_ok, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const KeyImpl* K = impl(k);
+  if (!K) return LORENZ_E_ARG;
+  if (first_bad_block) *first_bad_block = -1;
+  uint64_t ptb = 0, ctb = 0;
+  if (b0 < b1) slice_bytes(K, n, b0, b1, &ptb, &ctb);
+  lorenz_status s = check_range(K, n, b0, b1, ct, ctb, pt, ptb);
+  if (s != LORENZ_OK || b0 == b1) return s;
+  lorenz_result* d_res = nullptr;
+  if ((s = alloc_result(&d_res, st)) != LORENZ_OK) return s;
+  s = lorenz_decrypt_async(k, n, b0, b1, ct, pt, block_ok, d_res, stream);
+  lorenz_result h;
+  lorenz_status f = finish_sync(d_res, st, &h);
+  if (s != LORENZ_OK) return s;
+  if (first_bad_block && h.first_bad != ~0ULL) *first_bad_block = (int64_t)h.first_bad;
+  return f;
+}
+
+lorenz_status lorenz_verify(const lorenz_key* k, uint64_t n, uint64_t b0, uint64_t b1, const uint8_t* ct,
+                            int64_t* first_bad_block, uint8_t tag_xor[16], void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const KeyImpl* K = impl(k);
+  if (!K) return LORENZ_E_ARG;
+  if (first_bad_block) *first_bad_block = -1;
+  if (tag_xor) std::memset(tag_xor, 0, 16);
+  uint64_t ptb = 0, ctb = 0;
+  if (b0 < b1) slice_bytes(K, n, b0, b1, &ptb, &ctb);
+  lorenz_status s = check_range(K, n, b0, b1, ct, ctb, nullptr, 0);
+  if (s != LORENZ_OK || b0 == b1) return s;
+  lorenz_result* d_res = nullptr;
+  if ((s = alloc_result(&d_res, st)) != LORENZ_OK) return s;
+  s = lorenz_verify_async(k, n, b0, b1, ct, d_res, stream);
+  lorenz_result h;
+  lorenz_status f = finish_sync(d_res, st, &h);
+  if (s != LORENZ_OK) return s;
+  if (first_bad_block && h.first_bad != ~0ULL) *first_bad_block = (int64_t)h.first_bad;
+  if (tag_xor && f != LORENZ_E_CUDA) std::memcpy(tag_xor, h.tag_xor, 16);
+  return f;
+}
+
+lorenz_status lorenz_encrypt_batch(const lorenz_key* keys, uint32_t S, uint64_t n, const uint8_t* pts,
+                                   uint8_t* cts, uint8_t* tags, void* stream) {
+  if (!keys || S == 0) return LORENZ_E_ARG;
+  const KeyImpl* K0 = impl(&keys[0]);
+  if (!K0) return LORENZ_E_ARG;
+  for (uint32_t s = 1; s < S; ++s) {
+    const KeyImpl* Ks = impl(&keys[s]);
+    if (!Ks || std::memcmp(&Ks->prm, &K0->prm, sizeof K0->prm) != 0) return LORENZ_E_ARG;
+  }
+  const uint64_t nb = nblocks(K0, n), ctl = n + 16 * nb;
+  if (K0->prm.mode == LORENZ_FAST && nb > (1ULL << 32)) return LORENZ_E_ARG;
+  if ((n && (!pts || !aligned16(pts) || n % 16)) || !cts || !aligned16(cts) || !tags) return LORENZ_E_ARG;
+  if (overlap(pts, n * S, cts, ctl * S)) return LORENZ_E_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  lz::DevKey* d_keys = nullptr;
+  lz::DevKey* h_keys = nullptr;
+  if (!cuda_ok(cudaMallocHost(reinterpret_cast<void**>(&h_keys), sizeof(lz::DevKey) * S), "cudaMallocHost"))
+    return LORENZ_E_CUDA;
+  for (uint32_t s = 0; s < S; ++s) h_keys[s] = make_devkey(impl(&keys[s]));
+  lorenz_status ret = LORENZ_OK;
+  lorenz_result* d_res = nullptr;
+  do {
+    if (!cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&d_keys), sizeof(lz::DevKey) * S, st), "alloc keys")) {
+      ret = LORENZ_E_CUDA; break;
+    }
+    if (!cuda_ok(cudaMemcpyAsync(d_keys, h_keys, sizeof(lz::DevKey) * S, cudaMemcpyHostToDevice, st), "keys H2D") ||
+        !cuda_ok(cudaMemsetAsync(tags, 0, 16ull * S, st), "tags memset")) {
+      ret = LORENZ_E_CUDA; break;
+    }
+    if ((ret = alloc_result(&d_res, st)) != LORENZ_OK) break;
+    lz::DevConst C = make_const(K0, n, 0, nb * S);
+    C.batch = 1;
+    C.in_msg_stride = n;
+    C.out_msg_stride = ctl;
+    lz::DevKey dummy;
+    std::memset(&dummy, 0, sizeof dummy);
+    if (!cuda_ok(launch_chain<lz::OP_ENC>(C, dummy, d_keys, K0->prm.integrator, pts, cts, d_res, tags, nullptr, st),
+                 "batch launch")) {
+      ret = LORENZ_E_CUDA; break;
+    }
+  } while (0);
+  if (d_keys) cudaFreeAsync(d_keys, st);
+  if (d_res) {
+    lorenz_result h;
+    lorenz_status f = finish_sync(d_res, st, &h);
+    if (ret == LORENZ_OK) ret = f;
+  } else {
+    cudaStreamSynchronize(st);
+  }
+  cudaFreeHost(h_keys);
+  return ret;
+}
+
+// ---------------------------------------------------------------- host-buffer end to end
+namespace {
+struct HostPipe {
+  static constexpr int kStreams = 3;
+  cudaStream_t st[kStreams] = {nullptr, nullptr, nullptr};
+  cudaEvent_t ev[kStreams] = {nullptr, nullptr, nullptr};
+  bool init() {
+    static bool pool_set = false;
+    if (!pool_set) {  // keep freed stream-ordered memory cached across calls
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = ~0ULL;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+      }
+      pool_set = true;
+    }
+    for (int i = 0; i < kStreams; ++i) {
+      if (!cuda_ok(cudaStreamCreateWithFlags(&st[i], cudaStreamNonBlocking), "stream create")) return false;
+      if (!cuda_ok(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming), "event create")) return false;
+    }
+    return true;
+  }
+  // all streams wait for stream 0's work so far
+  void fan_out() {
+    cudaEventRecord(ev[0], st[0]);
+    for (int i = 1; i < kStreams; ++i) cudaStreamWaitEvent(st[i], ev[0], 0);
+  }
+  // stream 0 waits for every stream
+  void fan_in() {
+    for (int i = 1; i < kStreams; ++i) {
+      cudaEventRecord(ev[i], st[i]);
+      cudaStreamWaitEvent(st[0], ev[i], 0);
+    }
+  }
+  ~HostPipe() {
+    for (int i = 0; i < kStreams; ++i) {
+      if (st[i]) cudaStreamDestroy(st[i]);
+      if (ev[i]) cudaEventDestroy(ev[i]);
+    }
+  }
+};
+
+uint32_t auto_chunks(uint64_t nb, uint32_t req) {
+  uint64_t c = req ? req : 8;
+  if (c > nb) c = nb;
+  return (uint32_t)(c ? c : 1);
+}
+}  // namespace
+
+// Blocks [B0,B1) from host slices: chunked H2D -> kernel -> D2H over HostPipe's streams.
+static lorenz_status host_range(const lorenz_key* k, uint64_t n, uint64_t B0, uint64_t B1, const uint8_t* in_host,
+                                uint8_t* out_host, bool decrypt, lorenz_result* h_res, uint32_t n_chunks) {
+  const KeyImpl* K = impl(k);
+  if (!K) return LORENZ_E_ARG;
+  uint64_t ptb = 0, ctb = 0;
+  if (B0 < B1) slice_bytes(K, n, B0, B1, &ptb, &ctb);
+  const uint64_t inb = decrypt ? ctb : ptb, outb = decrypt ? ptb : ctb;
+  lorenz_status ret = check_range(K, n, B0, B1, in_host, inb, out_host, outb);
+  if (ret != LORENZ_OK || B0 == B1) return ret;
+  HostPipe P;
+  if (!P.init()) return LORENZ_E_CUDA;
+  uint8_t *d_in = nullptr, *d_out = nullptr, *d_ok = nullptr;
+  lorenz_result* d_res = nullptr;
+  cudaStream_t s0 = P.st[0];
+  if (!cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&d_in), inb ? inb : 16, s0), "alloc in") ||
+      !cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&d_out), outb ? outb : 16, s0), "alloc out") ||
+      (decrypt && !cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&d_ok), B1 - B0, s0), "alloc ok")))
+    ret = LORENZ_E_CUDA;
+  if (ret == LORENZ_OK) ret = alloc_result(&d_res, s0);
+  if (ret == LORENZ_OK) {
+    P.fan_out();
+    const uint32_t C = auto_chunks(B1 - B0, n_chunks);
+    const uint64_t Bsz = block_B(K, n);
+    for (uint32_t c = 0; c < C && ret == LORENZ_OK; ++c) {
+      const uint64_t b0 = B0 + (B1 - B0) * c / C, b1 = B0 + (B1 - B0) * (c + 1) / C;
+      if (b0 == b1) continue;
+      cudaStream_t st = P.st[c % HostPipe::kStreams];
+      uint64_t cp, cc;
+      slice_bytes(K, n, b0, b1, &cp, &cc);
+      const uint64_t poff = (b0 - B0) * Bsz, coff = poff + 16 * (b0 - B0);  // offsets inside the slice
+      const uint64_t ioff = decrypt ? coff : poff, ooff = decrypt ? poff : coff;
+      const uint64_t ib = decrypt ? cc : cp, ob = decrypt ? cp : cc;
+      if (ib && !cuda_ok(cudaMemcpyAsync(d_in + ioff, in_host + ioff, ib, cudaMemcpyHostToDevice, st), "H2D")) {
+        ret = LORENZ_E_CUDA; break;
+      }
+      ret = decrypt ? lorenz_decrypt_async(k, n, b0, b1, d_in + ioff, d_out + ooff, d_ok + (b0 - B0), d_res, st)
+                    : lorenz_encrypt_async(k, n, b0, b1, d_in + ioff, d_out + ooff, d_res, st);
+      if (ret == LORENZ_OK && ob &&
+          !cuda_ok(cudaMemcpyAsync(out_host + ooff, d_out + ooff, ob, cudaMemcpyDeviceToHost, st), "D2H"))
+        ret = LORENZ_E_CUDA;
+    }
+    P.fan_in();
+  }
+  if (d_in) cudaFreeAsync(d_in, s0);
+  if (d_out) cudaFreeAsync(d_out, s0);
+  if (d_ok) cudaFreeAsync(d_ok, s0);
+  if (d_res) {
+    lorenz_status f = finish_sync(d_res, s0, h_res);
+    if (ret == LORENZ_OK) ret = f;
+  } else {
+    cudaStreamSynchronize(s0);
+  }
+  if (decrypt && ret == LORENZ_E_INTEGRITY && outb) std::memset(out_host, 0, outb);  // never release it
+  return ret;
+}
+
+lorenz_status lorenz_encrypt_host(const lorenz_key* k, uint64_t n, uint64_t b0, uint64_t b1, const uint8_t* pt_host,
+                                  uint8_t* ct_host, uint8_t tag_xor[16], uint32_t n_chunks) {
+  if (tag_xor) std::memset(tag_xor, 0, 16);
+  lorenz_result h;
+  std::memset(&h, 0, sizeof h);
+  lorenz_status ret = host_range(k, n, b0, b1, pt_host, ct_host, false, &h, n_chunks);
+  if (ret == LORENZ_OK && tag_xor) std::memcpy(tag_xor, h.tag_xor, 16);
+  return ret;
+}
+
+lorenz_status lorenz_decrypt_host(const lorenz_key* k, uint64_t n, uint64_t b0, uint64_t b1, const uint8_t* ct_host,
+                                  uint8_t* pt_host, int64_t* first_bad_block, uint32_t n_chunks) {
+  if (first_bad_block) *first_bad_block = -1;
+  lorenz_result h;
+  std::memset(&h, 0, sizeof h);
+  h.first_bad = ~0ULL;
+  lorenz_status ret = host_range(k, n, b0, b1, ct_host, pt_host, true, &h, n_chunks);
+  if (first_bad_block && h.first_bad != ~0ULL) *first_bad_block = (int64_t)h.first_bad;
+  return ret;
+}
+
+}  // extern "C"

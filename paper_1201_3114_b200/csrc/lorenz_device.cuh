@@ -1,0 +1,529 @@
+// lorenz_device.cuh — device side of the per-block chaotic operation mode (sm_100a).
+//
+// One lane (thread) owns one block of the message: it derives the block's key
+// (§3.1, Eqs.2-7), then runs the block's characters through Steps 1-3
+// (§3.2) with the Lorenz state in registers, FP64 round-to-nearest and no
+// FMA (__dadd_rn/__dmul_rn are never contracted), in the operation order of
+// the same order the CPU oracle follows, so the outputs are
+// bit-identical. Bytes stream through a per-warp shared-memory stage with coalesced
+// 16-byte global loads/stores; warp shuffles reduce the per-block tags.
+#pragma once
+#include <cstdint>
+
+#include "../../include/lorenz.h"
+#include "sha256.cuh"
+
+namespace lz {
+
+// ------------------------------------------------------------------ launch data
+struct DevKey {          // one stream password (by value for one message, array for a batch)
+  uint32_t mid[8];       // FAST: SHA-256 midstate after the raw password's full 64-byte blocks
+  uint32_t fin[32];      // FAST: final SHA-256 block(s) of pw || BE32(b) || padding, b slot zeroed
+  uint32_t pw[6];        // STRONG: normalised password bytes as big-endian words, zero padded
+  uint32_t fin_blocks;   // FAST: 1 or 2
+  uint32_t b_off;        // FAST: byte offset of the BE32(b) slot inside fin
+  uint32_t pw_len;       // STRONG: 3..23
+  uint32_t pad_;
+};
+
+struct DevConst {
+  double sigma, rho, beta, h, h2, h6;  // exact bit patterns from the key
+  uint64_t n;                          // plaintext length of each message
+  uint64_t B;                          // block size (STRONG: n)
+  uint64_t b0;                         // first global block of this launch
+  uint64_t lanes;                      // lanes (= blocks) in this launch
+  uint64_t nb;                         // blocks per message (batch lane -> (message, block))
+  uint64_t in_msg_stride, out_msg_stride;
+  uint32_t n_it;                       // map iterations per character
+  uint32_t fast;                       // 1: per-block sub-keys
+  uint32_t batch;                      // 1: keys from the device array, tags per message
+  uint32_t pad_;
+};
+
+enum { OP_ENC = 0, OP_DEC = 1, OP_VERIFY = 2 };
+enum { ST_INTEGRITY = 1, ST_DIVERGENCE = 4 };
+
+constexpr int kCta = 128;              // 4 warps: one per SM sub-partition
+constexpr int kWarps = kCta / 32;
+constexpr int kWin = 64;               // characters per lane per staged window
+constexpr int kRow = kWin + 16;        // smem row stride: per-lane 16-B reads are conflict-free
+constexpr int kChunks = kWin / 16;
+
+// "LORENZCHAOS-MAC1" (Q15) as two little-endian words.
+constexpr uint64_t kSentLo = 0x48435A4E45524F4CULL;
+constexpr uint64_t kSentHi = 0x3143414D2D534F41ULL;
+
+__device__ __forceinline__ uint32_t sent_byte(uint32_t i) {
+  return (uint32_t)(((i < 8) ? (kSentLo >> (8 * i)) : (kSentHi >> (8 * (i - 8)))) & 0xFF);
+}
+
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+
+__device__ __forceinline__ double sel3(uint32_t i, double x, double y, double z) {
+  return i == 0 ? x : (i == 1 ? y : z);
+}
+
+// big-endian byte i (0-based, i < 24) of six words; i is warp-uniform in practice
+__device__ __forceinline__ uint32_t pw_byte(const uint32_t w[6], uint32_t i) {
+  uint32_t q = i >> 2, word = w[0];
+#pragma unroll
+  for (int k = 1; k < 6; ++k) word = (q == (uint32_t)k) ? w[k] : word;
+  return (word >> (24 - 8 * (i & 3))) & 0xFF;
+}
+
+// 10^e, e in [3, 8]: exact binary64 values (Theta's divisor)
+__device__ __forceinline__ double pow10_theta(uint32_t e) {
+  double v = 1e3;
+  v = (e == 4) ? 1e4 : v;
+  v = (e == 5) ? 1e5 : v;
+  v = (e == 6) ? 1e6 : v;
+  v = (e == 7) ? 1e7 : v;
+  v = (e == 8) ? 1e8 : v;
+  return v;
+}
+
+// 10^ceil(log10 2^{8(L+1)}) for L = 1..7 (g of P:209): 1e5,1e8,1e10,1e13,1e15,1e17,1e20
+__device__ __forceinline__ double g_divisor(uint32_t L) {
+  double v = 1e5;
+  v = (L == 2) ? 1e8 : v;
+  v = (L == 3) ? 1e10 : v;
+  v = (L == 4) ? 1e13 : v;
+  v = (L == 5) ? 1e15 : v;
+  v = (L == 6) ? 1e17 : v;
+  v = (L == 7) ? 1e20 : v;
+  return v;
+}
+
+// floor(|alpha| * 10^13) of the rounded product (Eq.8, Q8, Q9)
+__device__ __forceinline__ uint64_t quantise(double alpha) {
+  return __double2ull_rz(dmul(fabs(alpha), 1e13));
+}
+
+__device__ __forceinline__ uint32_t rbyte(uint64_t m, uint32_t omega) {
+  return (uint32_t)(m >> (8 * omega)) & 0xFF;
+}
+
+// ------------------------------------------------------------------ chain state
+struct Chain {
+  double x, y, z;          // r
+  double apx, apy, apz;    // a', added after every character
+  uint64_t m1, m2;         // floor(|alpha_1,2| 10^13) feeding Step 1
+  uint32_t mu1, mu2, mu3;
+  uint32_t om1, om2, om3;  // Eq.7
+  uint32_t k1, k2, k3;     // k1,k2 and k3 of Step 3
+};
+
+// Key schedule of one stream password. FAST derives the block password
+// SHA-256(pw || BE32 b)[0:18] from the midstate first (Q16). All hashes run
+// through one in-register compression inside a job loop (small code, no local memory).
+__device__ __forceinline__ void key_schedule(const DevKey& K, bool fast, uint32_t b, Chain& ch) {
+  uint32_t pw[6];
+  uint32_t np;
+  Sha256State s;
+  if (fast) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s.h[i] = K.mid[i];
+    const uint32_t q = K.b_off >> 2, sh = K.b_off & 3;
+#pragma unroll
+    for (int blk = 0; blk < 2; ++blk) {
+      if (blk < (int)K.fin_blocks) {
+        uint32_t w[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const uint32_t wi = 16 * blk + k;
+          uint32_t v = K.fin[16 * blk + k];
+          if (wi == q) v |= sh ? (b >> (8 * sh)) : b;
+          if (sh && wi == q + 1) v |= b << (8 * (4 - sh));
+          w[k] = v;
+        }
+        s.compress(w);
+      }
+    }
+    pw[0] = s.h[0]; pw[1] = s.h[1]; pw[2] = s.h[2]; pw[3] = s.h[3];
+    pw[4] = s.h[4] & 0xFFFF0000u; pw[5] = 0;
+    np = 18;
+  } else {
+#pragma unroll
+    for (int i = 0; i < 6; ++i) pw[i] = K.pw[i];
+    np = K.pw_len;
+  }
+
+  // Eqs.2-4: L = floor(n/3), little-endian digit groups + remainder bytes
+  const uint32_t L = np / 3, rem = np - 3 * L;
+  uint64_t g1 = 0, g2 = 0, g3 = 0;
+#pragma unroll
+  for (uint32_t j = 0; j < 7; ++j) {
+    if (j < L) {
+      g1 |= (uint64_t)pw_byte(pw, j) << (8 * j);
+      g2 |= (uint64_t)pw_byte(pw, L + j) << (8 * j);
+      g3 |= (uint64_t)pw_byte(pw, 2 * L + j) << (8 * j);
+    }
+  }
+  const uint64_t a1 = rem == 0 ? g1 : ((g1 << 8) | pw_byte(pw, 3 * L));
+  const uint64_t a2 = rem == 2 ? ((g2 << 8) | pw_byte(pw, 3 * L + 1)) : g2;
+  const uint64_t a3 = g3;
+
+  // a' = g(a)
+  const double gd = g_divisor(L);
+  ch.apx = __ddiv_rn(__ull2double_rn(a1), gd);
+  ch.apy = __ddiv_rn(__ull2double_rn(a2), gd);
+  ch.apz = __ddiv_rn(__ull2double_rn(a3), gd);
+
+  // jobs: 0 = SHA-256(pi_b) for k (Q12); 1..3 = lambda_i (Q10); 4..6 = Omega_i (Eq.7, Q11)
+  double lam1 = 0, lam2 = 0, lam3 = 0;
+  uint32_t hk = 0;
+  uint64_t ho1 = 0, ho2 = 0, ho3 = 0;
+#pragma unroll 1
+  for (uint32_t job = 0; job < 7; ++job) {
+    uint32_t w[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) w[k] = 0;
+    if (job == 0) {
+#pragma unroll
+      for (int k = 0; k < 6; ++k) w[k] = pw[k];
+      const uint32_t q = np >> 2, bit = 24 - 8 * (np & 3);
+#pragma unroll
+      for (int k = 0; k < 6; ++k) w[k] |= (q == (uint32_t)k) ? (0x80u << bit) : 0u;
+      w[15] = np * 8;
+    } else if (job <= 3) {
+      // 0x4C || BE64 a1 || BE64 a2 || BE64 a3 || u8 i || 0x80 ... || len=208
+      const uint32_t i = job;
+      w[0] = 0x4C000000u | (uint32_t)(a1 >> 40);
+      w[1] = (uint32_t)(a1 >> 8);
+      w[2] = ((uint32_t)a1 << 24) | (uint32_t)(a2 >> 40);
+      w[3] = (uint32_t)(a2 >> 8);
+      w[4] = ((uint32_t)a2 << 24) | (uint32_t)(a3 >> 40);
+      w[5] = (uint32_t)(a3 >> 8);
+      w[6] = ((uint32_t)a3 << 24) | (i << 16) | 0x8000u;
+      w[15] = 26 * 8;
+    } else {
+      // BE64(i a1) || BE64(i a2) || BE64(i a3), products mod 2^64, len=192
+      const uint64_t i = job - 3;
+      const uint64_t p1 = i * a1, p2 = i * a2, p3 = i * a3;
+      w[0] = (uint32_t)(p1 >> 32); w[1] = (uint32_t)p1;
+      w[2] = (uint32_t)(p2 >> 32); w[3] = (uint32_t)p2;
+      w[4] = (uint32_t)(p3 >> 32); w[5] = (uint32_t)p3;
+      w[6] = 0x80000000u;
+      w[15] = 24 * 8;
+    }
+    s.init();
+    s.compress(w);
+    const uint64_t h64 = ((uint64_t)s.h[0] << 32) | s.h[1];
+    if (job == 0) {
+      hk = s.h[0];
+    } else if (job <= 3) {
+      // lambda_i = lo_i + (double(h) 2^-64)(hi_i - lo_i)  (P:216 ranges; Q10)
+      const double lo = job == 1 ? -15.67 : (job == 2 ? -11.28 : 0.090);
+      const double hi = job == 1 ? 16.01 : (job == 2 ? 16.01 : 62.000);
+      const double t = dmul(__ull2double_rn(h64), 0x1p-64);
+      const double lam = dadd(lo, dmul(t, dsub(hi, lo)));
+      if (job == 1) lam1 = lam; else if (job == 2) lam2 = lam; else lam3 = lam;
+    } else {
+      if (job == 4) ho1 = h64; else if (job == 5) ho2 = h64; else ho3 = h64;
+    }
+  }
+  // k_i = 3 + H[i-1] mod 2; k3 of Step 3 = 1 + H[3] mod 6 (Q12)
+  const uint32_t k1i = 3 + ((hk >> 24) & 1), k2i = 3 + ((hk >> 16) & 1), k3i = 3 + ((hk >> 8) & 1);
+  ch.k1 = k1i;
+  ch.k2 = k2i;
+  ch.k3 = 1 + (hk & 0xFF) % 6;
+  ch.om1 = (uint32_t)(ho1 % k1i);
+  ch.om2 = (uint32_t)(ho2 % k2i);
+  ch.om3 = (uint32_t)(ho3 % k3i);
+  // mu, over the integers, reduced mod 3
+  const uint64_t r1 = a1 % 3, r2 = a2 % 3, r3 = a3 % 3;
+  ch.mu1 = (uint32_t)((r1 + r2 + r3) % 3);
+  ch.mu2 = (uint32_t)((r1 * r2 + r3) % 3);
+  ch.mu3 = (uint32_t)((r1 + r2 * r3) % 3);
+  // r0 = a' + lambda (Eq.5); alpha0 = r0[mu] (Eq.6, n = 0, Q14)
+  ch.x = dadd(ch.apx, lam1);
+  ch.y = dadd(ch.apy, lam2);
+  ch.z = dadd(ch.apz, lam3);
+  ch.m1 = quantise(sel3(ch.mu1, ch.x, ch.y, ch.z));
+  ch.m2 = quantise(sel3(ch.mu2, ch.x, ch.y, ch.z));
+}
+
+// n_it steps of the Lorenz map. RK4 in the canonical order of DESIGN.md §2
+// (43 DADD + 32 DMUL per step, no FMA), or forward Euler (NEXT-1).
+template <int INTEG>
+__device__ __forceinline__ void integrate(double& x, double& y, double& z, const DevConst& C) {
+  const double S = C.sigma, R = C.rho, Bt = C.beta, h = C.h, h2 = C.h2, h6 = C.h6;
+#pragma unroll 1
+  for (uint32_t it = 0; it < C.n_it; ++it) {
+    if (INTEG == LORENZ_RK4) {
+      const double k1x = dmul(S, dsub(y, x));
+      const double k1y = dsub(dsub(dmul(R, x), y), dmul(x, z));
+      const double k1z = dsub(dmul(x, y), dmul(Bt, z));
+      const double ax = dadd(x, dmul(h2, k1x)), ay = dadd(y, dmul(h2, k1y)), az = dadd(z, dmul(h2, k1z));
+      const double k2x = dmul(S, dsub(ay, ax));
+      const double k2y = dsub(dsub(dmul(R, ax), ay), dmul(ax, az));
+      const double k2z = dsub(dmul(ax, ay), dmul(Bt, az));
+      const double bx = dadd(x, dmul(h2, k2x)), by = dadd(y, dmul(h2, k2y)), bz = dadd(z, dmul(h2, k2z));
+      const double k3x = dmul(S, dsub(by, bx));
+      const double k3y = dsub(dsub(dmul(R, bx), by), dmul(bx, bz));
+      const double k3z = dsub(dmul(bx, by), dmul(Bt, bz));
+      const double cx = dadd(x, dmul(h, k3x)), cy = dadd(y, dmul(h, k3y)), cz = dadd(z, dmul(h, k3z));
+      const double k4x = dmul(S, dsub(cy, cx));
+      const double k4y = dsub(dsub(dmul(R, cx), cy), dmul(cx, cz));
+      const double k4z = dsub(dmul(cx, cy), dmul(Bt, cz));
+      double sx = dadd(k1x, k2x), sy = dadd(k1y, k2y), sz = dadd(k1z, k2z);
+      sx = dadd(sx, k2x); sy = dadd(sy, k2y); sz = dadd(sz, k2z);
+      sx = dadd(sx, k3x); sy = dadd(sy, k3y); sz = dadd(sz, k3z);
+      sx = dadd(sx, k3x); sy = dadd(sy, k3y); sz = dadd(sz, k3z);
+      sx = dadd(sx, k4x); sy = dadd(sy, k4y); sz = dadd(sz, k4z);
+      x = dadd(x, dmul(h6, sx));
+      y = dadd(y, dmul(h6, sy));
+      z = dadd(z, dmul(h6, sz));
+    } else {
+      const double fx = dmul(S, dsub(y, x));
+      const double fy = dsub(dsub(dmul(R, x), y), dmul(x, z));
+      const double fz = dsub(dmul(x, y), dmul(Bt, z));
+      x = dadd(x, dmul(fx, h));
+      y = dadd(y, dmul(fy, h));
+      z = dadd(z, dmul(fz, h));
+    }
+  }
+}
+
+// Steps 2-3 after the character's plaintext byte p is known (Q13).
+// Returns false if the guard of Q18 fails.
+template <int INTEG>
+__device__ __forceinline__ bool advance(Chain& ch, uint32_t p, const DevConst& C) {
+  // Step 2: Theta = P_i / 10^{3+Omega_3} (correctly rounded, Q19) added to r[mu_3]
+  const double theta = __ddiv_rn(__uint2double_rn(p), pow10_theta(3 + ch.om3));
+  const double t = dadd(sel3(ch.mu3, ch.x, ch.y, ch.z), theta);
+  ch.x = ch.mu3 == 0 ? t : ch.x;
+  ch.y = ch.mu3 == 1 ? t : ch.y;
+  ch.z = ch.mu3 == 2 ? t : ch.z;
+  integrate<INTEG>(ch.x, ch.y, ch.z, C);
+  const bool ok = (fabs(ch.x) <= 100.0) & (fabs(ch.y) <= 100.0) & (ch.z >= -50.0) & (ch.z <= 150.0);
+  // Step 3: alpha_i = r[mu_i]; R_i = R(alpha_i, Omega_i); mu, Omega += R_i; r += a'
+  const uint64_t m1 = quantise(sel3(ch.mu1, ch.x, ch.y, ch.z));
+  const uint64_t m2 = quantise(sel3(ch.mu2, ch.x, ch.y, ch.z));
+  const uint64_t m3 = quantise(sel3(ch.mu3, ch.x, ch.y, ch.z));
+  const uint32_t R1 = rbyte(m1, ch.om1), R2 = rbyte(m2, ch.om2), R3 = rbyte(m3, ch.om3);
+  ch.mu1 = (ch.mu1 + R1) % 3;
+  ch.mu2 = (ch.mu2 + R2) % 3;
+  ch.mu3 = (ch.mu3 + R3) % 3;
+  ch.om1 = (ch.om1 + R1) % ch.k1;
+  ch.om2 = (ch.om2 + R2) % ch.k2;
+  ch.om3 = (ch.om3 + R3) % ch.k3;
+  ch.m1 = m1;
+  ch.m2 = m2;
+  ch.x = dadd(ch.x, ch.apx);
+  ch.y = dadd(ch.y, ch.apy);
+  ch.z = dadd(ch.z, ch.apz);
+  return ok;
+}
+
+__device__ __forceinline__ uint64_t warp_max_u64(uint64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const uint64_t u = __shfl_xor_sync(0xffffffffu, v, o);
+    v = u > v ? u : v;
+  }
+  return v;
+}
+
+__device__ __forceinline__ uint4 ld_stream(const uint8_t* p) {
+  return __ldcs(reinterpret_cast<const uint4*>(p));
+}
+__device__ __forceinline__ void st_stream(uint8_t* p, uint4 v) {
+  __stcs(reinterpret_cast<uint4*>(p), v);
+}
+
+// ------------------------------------------------------------------ the kernel
+// OP: OP_ENC / OP_DEC / OP_VERIFY. One lane per block; warps are independent
+// (only __syncwarp), so the CTA never waits on its slowest warp.
+template <int OP, int INTEG>
+__global__ void __launch_bounds__(kCta)
+    lorenz_chain_kernel(const DevConst C, const DevKey K1, const DevKey* __restrict__ Kb,
+                        const uint8_t* __restrict__ in, uint8_t* __restrict__ out,
+                        lorenz_result* __restrict__ res, uint8_t* __restrict__ tags_batch,
+                        uint8_t* __restrict__ block_ok) {
+  __shared__ __align__(16) uint8_t stage[kWarps * 32 * kRow];
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint8_t* wst = stage + warp * 32 * kRow;
+  const uint64_t g = (uint64_t)blockIdx.x * kCta + threadIdx.x;
+  const bool active = g < C.lanes;
+
+  // lane -> (message s, global block bl)
+  uint64_t s = 0, bl = C.b0 + g;
+  if (C.batch) { s = g / C.nb; bl = g - s * C.nb; }
+  uint64_t len = 0;
+  if (active) {
+    const uint64_t start = C.fast ? bl * C.B : 0;
+    len = C.fast ? ((C.n - start) < C.B ? (C.n - start) : C.B) : C.n;
+  }
+  const uint64_t total = active ? len + 16 : 0;
+  const uint64_t rb = bl - C.b0;  // block index inside the slice
+  const uint8_t* irow = in + s * C.in_msg_stride + rb * (OP == OP_ENC ? C.B : C.B + 16);
+  uint8_t* orow = out + s * C.out_msg_stride + rb * (OP == OP_ENC ? C.B + 16 : C.B);
+  if (!active) { irow = in; orow = out; }
+
+  Chain ch;
+  if (active) {
+    const DevKey& K = C.batch ? Kb[s] : K1;
+    key_schedule(K, C.fast != 0, (uint32_t)bl, ch);
+  }
+
+  bool guard_ok = true, bad = false;
+  uint64_t tlo = 0, thi = 0;  // last 16 ciphertext bytes = the block tag
+  const uint64_t wtotal = warp_max_u64(total);
+
+  for (uint64_t w0 = 0; w0 < wtotal; w0 += kWin) {
+    // ---- stage in: 32 rows x kWin bytes, coalesced 16-B chunks ----
+#pragma unroll
+    for (int it = 0; it < kChunks; ++it) {
+      const uint32_t q = it * 32 + lane, row = q / kChunks, c = q % kChunks;
+      const uint8_t* r_in = (const uint8_t*)__shfl_sync(0xffffffffu, (unsigned long long)irow, row);
+      const uint64_t r_len = __shfl_sync(0xffffffffu, len, row);
+      const uint64_t r_tot = __shfl_sync(0xffffffffu, total, row);
+      const uint64_t pos = w0 + 16 * c;
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if (pos < r_tot) {
+        const uint64_t r_src = (OP == OP_ENC) ? r_len : r_tot;  // bytes readable from memory
+        if (pos + 16 <= r_src) {
+          v = ld_stream(r_in + pos);
+        } else if (OP == OP_ENC && pos >= r_len && ((r_len & 15) == 0)) {
+          v = make_uint4((uint32_t)kSentLo, (uint32_t)(kSentLo >> 32), (uint32_t)kSentHi,
+                         (uint32_t)(kSentHi >> 32));
+        } else {
+          uint32_t wv[4] = {0, 0, 0, 0};
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const uint64_t j = pos + i;
+            uint32_t bv = 0;
+            if (j < r_src) bv = r_in[j];
+            else if (OP == OP_ENC && j < r_tot) bv = sent_byte((uint32_t)(j - r_len));
+            wv[i >> 2] |= bv << (8 * (i & 3));
+          }
+          v = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+        }
+      }
+      *reinterpret_cast<uint4*>(wst + row * kRow + 16 * c) = v;
+    }
+    __syncwarp();
+
+    // ---- the chain over this lane's characters [w0, min(w0+kWin, total)) ----
+    if (w0 < total) {
+      const uint64_t wend = (w0 + kWin < total) ? w0 + kWin : total;
+      for (uint64_t j0 = w0; j0 < wend; j0 += 16) {
+        uint4* cell = reinterpret_cast<uint4*>(wst + lane * kRow + (j0 - w0));
+        const uint4 v = *cell;
+        uint64_t ilo = (uint64_t)v.x | ((uint64_t)v.y << 32), ihi = (uint64_t)v.z | ((uint64_t)v.w << 32);
+        uint64_t olo = 0, ohi = 0;
+        const uint32_t cnt = (uint32_t)((wend - j0) < 16 ? (wend - j0) : 16);
+        for (uint32_t i = 0; i < cnt; ++i) {
+          const uint64_t j = j0 + i;
+          const uint32_t xin = (uint32_t)ilo & 0xFF;
+          ilo = (ilo >> 8) | (ihi << 56);
+          ihi >>= 8;
+          // Step 1 (Eqs.8-10): keystream sum_{i=1,2} R(alpha_i, Omega_i)
+          const uint32_t ks = rbyte(ch.m1, ch.om1) + rbyte(ch.m2, ch.om2);
+          uint32_t yout, p, cbyte;
+          if (OP == OP_ENC) {
+            yout = (xin + ks) & 0xFF; p = xin; cbyte = yout;
+          } else {
+            yout = (xin - ks) & 0xFF; p = yout; cbyte = xin;
+            if (j >= len) bad |= (yout != sent_byte((uint32_t)(j - len)));
+          }
+          olo = (olo >> 8) | (ohi << 56);
+          ohi = (ohi >> 8) | ((uint64_t)yout << 56);
+          tlo = (tlo >> 8) | (thi << 56);
+          thi = (thi >> 8) | ((uint64_t)cbyte << 56);
+          if (j + 1 == total) break;  // the last character is not advanced (Q20)
+          guard_ok &= advance<INTEG>(ch, p, C);
+        }
+        if (cnt < 16) {  // left-align a partial chunk
+          const uint32_t sh = 8 * (16 - cnt);
+          if (sh >= 64) { olo = ohi >> (sh - 64); ohi = 0; }
+          else { olo = (olo >> sh) | (ohi << (64 - sh)); ohi >>= sh; }
+        }
+        *cell = make_uint4((uint32_t)olo, (uint32_t)(olo >> 32), (uint32_t)ohi, (uint32_t)(ohi >> 32));
+      }
+    }
+    __syncwarp();
+
+    // ---- stage out ----
+    if (OP != OP_VERIFY) {
+#pragma unroll
+      for (int it = 0; it < kChunks; ++it) {
+        const uint32_t q = it * 32 + lane, row = q / kChunks, c = q % kChunks;
+        uint8_t* r_out = (uint8_t*)__shfl_sync(0xffffffffu, (unsigned long long)orow, row);
+        const uint64_t r_len = __shfl_sync(0xffffffffu, len, row);
+        const uint64_t r_tot = __shfl_sync(0xffffffffu, total, row);
+        const uint64_t r_dst = (OP == OP_ENC) ? r_tot : r_len;
+        const uint64_t pos = w0 + 16 * c;
+        if (r_tot && pos < r_dst) {
+          const uint4 v = *reinterpret_cast<const uint4*>(wst + row * kRow + 16 * c);
+          if (pos + 16 <= r_dst) {
+            st_stream(r_out + pos, v);
+          } else {
+            const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              if (pos + i < r_dst) r_out[pos + i] = (uint8_t)(wv[i >> 2] >> (8 * (i & 3)));
+          }
+        }
+      }
+    }
+    __syncwarp();
+  }
+
+  // ---- per-block verdicts and the tag combine ----
+  if (active) {
+    if (!guard_ok) atomicOr(&res->status, (uint32_t)ST_DIVERGENCE);
+    if (OP != OP_ENC) {
+      if (bad) {
+        atomicMin((unsigned long long*)&res->first_bad, (unsigned long long)bl);
+        atomicOr(&res->status, (uint32_t)ST_INTEGRITY);
+        if (OP == OP_DEC)  // never release unauthenticated plaintext
+          for (uint64_t j = 0; j < len; ++j) orow[j] = 0;
+      }
+      if (block_ok) block_ok[rb] = bad ? 0 : 1;
+    }
+  }
+  if (C.batch) {
+    if (active) {
+      unsigned long long* t = reinterpret_cast<unsigned long long*>(tags_batch + 16 * s);
+      atomicXor(t, (unsigned long long)tlo);
+      atomicXor(t + 1, (unsigned long long)thi);
+    }
+  } else {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      tlo ^= __shfl_xor_sync(0xffffffffu, tlo, o);
+      thi ^= __shfl_xor_sync(0xffffffffu, thi, o);
+    }
+    if (lane == 0 && (tlo | thi)) {
+      unsigned long long* t = reinterpret_cast<unsigned long long*>(res->tag_xor);
+      atomicXor(t, (unsigned long long)tlo);
+      atomicXor(t + 1, (unsigned long long)thi);
+    }
+  }
+}
+
+// Zero the plaintext slice if the launch found an integrity failure (async decrypt
+// without per-block verdicts: unauthenticated plaintext is never released).
+__global__ void zero_if_failed_kernel(const lorenz_result* __restrict__ res, uint8_t* __restrict__ pt,
+                                      uint64_t nbytes) {
+  if (!(res->status & ST_INTEGRITY)) return;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nbytes;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    pt[i] = 0;
+}
+
+__global__ void result_init_kernel(lorenz_result* res) {
+  if (threadIdx.x == 0) {
+    *reinterpret_cast<unsigned long long*>(res->tag_xor) = 0;
+    *reinterpret_cast<unsigned long long*>(res->tag_xor + 8) = 0;
+    res->first_bad = ~0ULL;
+    res->status = 0;
+    res->reserved = 0;
+  }
+}
+
+}  // namespace lz

@@ -1,0 +1,268 @@
+"""Thin Python binding of include/lorenz.h (liblorenz.so): same names, marshalling only.
+
+Every step of the cipher runs in the CUDA kernels of ``csrc/``; this module only
+turns Python objects (bytes, torch tensors, streams) into the C ABI's pointers and
+sizes. There is no CPU fallback: if liblorenz.so is missing, importing
+:func:`lib` raises.
+
+Device buffers are torch uint8 CUDA tensors (or raw device addresses as ints);
+streams default to torch's current stream.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "csrc", "liblorenz.so")
+
+OK, E_INTEGRITY, E_ARG, E_PASSWORD, E_LENGTH, E_DIVERGENCE, E_CUDA = range(7)
+STRONG, FAST = 0, 1
+RK4, EULER = 0, 1
+TAG_BYTES = 16
+KEY_BYTES = 384
+
+EXPORTS = ["lorenz_abi_version", "lorenz_last_error", "lorenz_status_string", "lorenz_keysetup",
+           "lorenz_key_params", "lorenz_num_blocks", "lorenz_ct_len", "lorenz_pt_len",
+           "lorenz_encrypt", "lorenz_decrypt", "lorenz_verify", "lorenz_result_init_async",
+           "lorenz_encrypt_async", "lorenz_decrypt_async", "lorenz_verify_async",
+           "lorenz_encrypt_batch", "lorenz_encrypt_host", "lorenz_decrypt_host"]
+
+
+class lorenz_params(C.Structure):
+    _fields_ = [("mode", C.c_uint32), ("n_it", C.c_uint32), ("dt_code", C.c_uint32),
+                ("block_size", C.c_uint32), ("integrator", C.c_uint32)]
+
+
+class lorenz_key(C.Structure):
+    _fields_ = [("opaque", C.c_uint8 * KEY_BYTES)]
+
+
+class lorenz_result(C.Structure):
+    _fields_ = [("tag_xor", C.c_uint8 * 16), ("first_bad", C.c_uint64), ("status", C.c_uint32),
+                ("reserved", C.c_uint32)]
+
+
+class LorenzError(RuntimeError):
+    def __init__(self, status: int, where: str = ""):
+        msg = lib().lorenz_status_string(status).decode()
+        if status == E_CUDA:
+            msg += ": " + lib().lorenz_last_error().decode()
+        super().__init__(f"{where}: {msg} (status {status})")
+        self.status = status
+
+
+_lib = None
+
+
+def lib():
+    """Load liblorenz.so (fails loudly when the CUDA library was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
+                              f"g.build()'` (nvcc, sm_100a). There is no CPU fallback.")
+        L = C.CDLL(LIB_PATH)
+        vp, u64, u32, sz = C.c_void_p, C.c_uint64, C.c_uint32, C.c_size_t
+        kp = C.POINTER(lorenz_key)
+        L.lorenz_abi_version.restype = C.c_int
+        L.lorenz_last_error.restype = C.c_char_p
+        L.lorenz_status_string.restype = C.c_char_p
+        L.lorenz_status_string.argtypes = [C.c_int]
+        L.lorenz_keysetup.argtypes = [C.c_char_p, sz, C.POINTER(lorenz_params), kp]
+        L.lorenz_key_params.argtypes = [kp, C.POINTER(lorenz_params)]
+        L.lorenz_num_blocks.argtypes = [kp, u64]
+        L.lorenz_num_blocks.restype = u64
+        L.lorenz_ct_len.argtypes = [kp, u64]
+        L.lorenz_ct_len.restype = u64
+        L.lorenz_pt_len.argtypes = [kp, u64, C.POINTER(u64)]
+        L.lorenz_encrypt.argtypes = [kp, u64, u64, u64, vp, vp, vp, vp]
+        L.lorenz_decrypt.argtypes = [kp, u64, u64, u64, vp, vp, C.POINTER(C.c_int64), vp, vp]
+        L.lorenz_verify.argtypes = [kp, u64, u64, u64, vp, C.POINTER(C.c_int64), vp, vp]
+        L.lorenz_result_init_async.argtypes = [vp, vp]
+        L.lorenz_encrypt_async.argtypes = [kp, u64, u64, u64, vp, vp, vp, vp]
+        L.lorenz_decrypt_async.argtypes = [kp, u64, u64, u64, vp, vp, vp, vp, vp]
+        L.lorenz_verify_async.argtypes = [kp, u64, u64, u64, vp, vp, vp]
+        L.lorenz_encrypt_batch.argtypes = [kp, u32, u64, vp, vp, vp, vp]
+        L.lorenz_encrypt_host.argtypes = [kp, u64, u64, u64, vp, vp, vp, u32]
+        L.lorenz_decrypt_host.argtypes = [kp, u64, u64, u64, vp, vp, C.POINTER(C.c_int64), u32]
+        for name in EXPORTS:
+            if name not in ("lorenz_abi_version", "lorenz_last_error", "lorenz_status_string",
+                            "lorenz_num_blocks", "lorenz_ct_len"):
+                getattr(L, name).restype = C.c_int
+        _lib = L
+    return _lib
+
+
+def _check(st: int, where: str):
+    if st != OK:
+        raise LorenzError(st, where)
+
+
+def _ptr(x) -> int | None:
+    """Device address of a torch tensor (must be contiguous) or a raw int; None -> NULL."""
+    if x is None:
+        return None
+    if isinstance(x, int):
+        return x
+    if not x.is_contiguous():
+        raise ValueError("buffer must be contiguous")
+    return x.data_ptr()
+
+
+def _stream(stream) -> int | None:
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+@dataclass
+class Key:
+    """A lorenz_key (384-byte POD) plus its effective params."""
+    raw: lorenz_key
+
+    @property
+    def params(self) -> lorenz_params:
+        p = lorenz_params()
+        _check(lib().lorenz_key_params(C.byref(self.raw), C.byref(p)), "lorenz_key_params")
+        return p
+
+    def num_blocks(self, n: int) -> int:
+        return lorenz_num_blocks(self, n)
+
+    def ct_len(self, n: int) -> int:
+        return lorenz_ct_len(self, n)
+
+    @property
+    def block_size(self) -> int:
+        return self.params.block_size
+
+
+def lorenz_keysetup(pw: bytes, mode: int = FAST, n_it: int = 0, dt_code: int = 0, block_size: int = 0,
+                    integrator: int = RK4) -> Key:
+    k = lorenz_key()
+    p = lorenz_params(mode, n_it, dt_code, block_size, integrator)
+    _check(lib().lorenz_keysetup(bytes(pw), len(pw), C.byref(p), C.byref(k)), "lorenz_keysetup")
+    return Key(k)
+
+
+def lorenz_num_blocks(key: Key, n: int) -> int:
+    return lib().lorenz_num_blocks(C.byref(key.raw), n)
+
+
+def lorenz_ct_len(key: Key, n: int) -> int:
+    return lib().lorenz_ct_len(C.byref(key.raw), n)
+
+
+def lorenz_pt_len(key: Key, ct_len: int) -> int:
+    out = C.c_uint64()
+    _check(lib().lorenz_pt_len(C.byref(key.raw), ct_len, C.byref(out)), "lorenz_pt_len")
+    return out.value
+
+
+def lorenz_encrypt(key: Key, n: int, b0: int, b1: int, pt, ct, stream=None) -> bytes:
+    """Encrypt global blocks [b0,b1); pt/ct are the slice starts. Returns the tag XOR."""
+    tag = (C.c_uint8 * 16)()
+    _check(lib().lorenz_encrypt(C.byref(key.raw), n, b0, b1, _ptr(pt), _ptr(ct), tag, _stream(stream)),
+           "lorenz_encrypt")
+    return bytes(tag)
+
+
+def lorenz_decrypt(key: Key, n: int, b0: int, b1: int, ct, pt, block_ok=None, stream=None,
+                   raise_on_integrity: bool = False):
+    """Returns (status, first_bad_block): status OK or E_INTEGRITY (others raise)."""
+    fb = C.c_int64(-1)
+    st = lib().lorenz_decrypt(C.byref(key.raw), n, b0, b1, _ptr(ct), _ptr(pt), C.byref(fb), _ptr(block_ok),
+                              _stream(stream))
+    if st != OK and (st != E_INTEGRITY or raise_on_integrity):
+        raise LorenzError(st, "lorenz_decrypt")
+    return st, fb.value
+
+
+def lorenz_verify(key: Key, n: int, b0: int, b1: int, ct, stream=None):
+    """Returns (status, first_bad_block, tag_xor)."""
+    fb = C.c_int64(-1)
+    tag = (C.c_uint8 * 16)()
+    st = lib().lorenz_verify(C.byref(key.raw), n, b0, b1, _ptr(ct), C.byref(fb), tag, _stream(stream))
+    if st not in (OK, E_INTEGRITY):
+        raise LorenzError(st, "lorenz_verify")
+    return st, fb.value, bytes(tag)
+
+
+def lorenz_result_init_async(res, stream=None):
+    _check(lib().lorenz_result_init_async(_ptr(res), _stream(stream)), "lorenz_result_init_async")
+
+
+def lorenz_encrypt_async(key: Key, n: int, b0: int, b1: int, pt, ct, res, stream=None):
+    _check(lib().lorenz_encrypt_async(C.byref(key.raw), n, b0, b1, _ptr(pt), _ptr(ct), _ptr(res),
+                                      _stream(stream)), "lorenz_encrypt_async")
+
+
+def lorenz_decrypt_async(key: Key, n: int, b0: int, b1: int, ct, pt, res, block_ok=None, stream=None):
+    _check(lib().lorenz_decrypt_async(C.byref(key.raw), n, b0, b1, _ptr(ct), _ptr(pt), _ptr(block_ok),
+                                      _ptr(res), _stream(stream)), "lorenz_decrypt_async")
+
+
+def lorenz_verify_async(key: Key, n: int, b0: int, b1: int, ct, res, stream=None):
+    _check(lib().lorenz_verify_async(C.byref(key.raw), n, b0, b1, _ptr(ct), _ptr(res), _stream(stream)),
+           "lorenz_verify_async")
+
+
+def lorenz_encrypt_batch(keys: list[Key], n: int, pts, cts, tags, stream=None):
+    arr = (lorenz_key * len(keys))(*[k.raw for k in keys])
+    _check(lib().lorenz_encrypt_batch(arr, len(keys), n, _ptr(pts), _ptr(cts), _ptr(tags), _stream(stream)),
+           "lorenz_encrypt_batch")
+
+
+def _host_ptr(buf) -> int | None:
+    if buf is None or isinstance(buf, int):
+        return buf
+    if hasattr(buf, "data_ptr"):
+        if buf.is_cuda:
+            raise ValueError("host buffer expected")
+        return buf.data_ptr()
+    import numpy as np
+    if not isinstance(buf, np.ndarray) or not buf.flags.c_contiguous:
+        raise TypeError("pass a contiguous numpy array, a CPU torch tensor, or an address")
+    return buf.ctypes.data if buf.size else None
+
+
+def lorenz_encrypt_host(key: Key, n: int, b0: int, b1: int, pt_host, ct_host, n_chunks: int = 0) -> bytes:
+    """End to end from host slices (pinned for overlap). Returns the tag XOR of [b0,b1)."""
+    tag = (C.c_uint8 * 16)()
+    _check(lib().lorenz_encrypt_host(C.byref(key.raw), n, b0, b1, _host_ptr(pt_host), _host_ptr(ct_host), tag,
+                                     n_chunks), "lorenz_encrypt_host")
+    return bytes(tag)
+
+
+def lorenz_decrypt_host(key: Key, n: int, b0: int, b1: int, ct_host, pt_host, n_chunks: int = 0):
+    """Returns (status, first_bad_block); the host plaintext slice is zeroed on failure."""
+    fb = C.c_int64(-1)
+    st = lib().lorenz_decrypt_host(C.byref(key.raw), n, b0, b1, _host_ptr(ct_host), _host_ptr(pt_host),
+                                   C.byref(fb), n_chunks)
+    if st not in (OK, E_INTEGRITY):
+        raise LorenzError(st, "lorenz_decrypt_host")
+    return st, fb.value
+
+
+# ---------------------------------------------------------------- conveniences over whole messages
+def encrypt(key: Key, pt, stream=None):
+    """Encrypt a whole message held in a CUDA uint8 tensor. Returns (ct tensor, tag bytes)."""
+    import torch
+    n = pt.numel()
+    ct = torch.empty(lorenz_ct_len(key, n), dtype=torch.uint8, device=pt.device)
+    tag = lorenz_encrypt(key, n, 0, lorenz_num_blocks(key, n), pt if n else None, ct, stream)
+    return ct, tag
+
+
+def decrypt(key: Key, ct, stream=None):
+    """Decrypt a whole ciphertext (CUDA uint8 tensor). Returns (pt tensor, status, first_bad)."""
+    import torch
+    n = lorenz_pt_len(key, ct.numel())
+    pt = torch.empty(max(n, 1), dtype=torch.uint8, device=ct.device)
+    st, fb = lorenz_decrypt(key, n, 0, lorenz_num_blocks(key, n), ct, pt if n else None, stream=stream)
+    return pt[:n], st, fb

@@ -1,0 +1,101 @@
+"""CPU-side checks of the C-ABI library (no GPU): it loads, exports every symbol that
+include/lorenz.h declares, and its host-only helpers (key setup, length arithmetic,
+argument validation) behave as documented. No compute call is made here.
+"""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "lorenz.h")
+
+
+@pytest.fixture(scope="module")
+def L():
+    from paper_1201_3114_b200 import build, lorenz
+    build.build()
+    lorenz.lib()
+    return lorenz
+
+
+def declared_symbols():
+    txt = open(HEADER).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(lorenz_[a-z0-9_]+)\s*\(", txt)))
+
+
+def test_exports_every_declared_symbol(L):
+    syms = declared_symbols()
+    assert len(syms) >= 17
+    so = C.CDLL(L.LIB_PATH)
+    for s in syms:
+        assert hasattr(so, s), s
+    assert set(L.EXPORTS) == set(syms)
+    assert L.lib().lorenz_abi_version() == 1
+
+
+def test_keysetup_deterministic_and_validated(L):
+    a = L.lorenz_keysetup(b"password123", mode=L.FAST)
+    b = L.lorenz_keysetup(b"password123", mode=L.FAST)
+    assert bytes(a.raw.opaque) == bytes(b.raw.opaque)
+    p = a.params
+    assert (p.mode, p.n_it, p.dt_code, p.block_size, p.integrator) == (L.FAST, 100, 0, 1024, L.RK4)
+    s = L.lorenz_keysetup(b"password123", mode=L.STRONG)
+    assert s.params.n_it == 3000
+    with pytest.raises(L.LorenzError) as e:
+        L.lorenz_keysetup(b"ab")
+    assert e.value.status == L.E_PASSWORD
+    for bad in (dict(block_size=1000), dict(block_size=1032), dict(dt_code=4), dict(integrator=2),
+                dict(mode=2)):
+        with pytest.raises(L.LorenzError) as e:
+            L.lorenz_keysetup(b"password", **bad)
+        assert e.value.status == L.E_ARG
+
+
+def test_length_arithmetic_matches_oracle(L, ref):
+    for mode in (L.FAST, L.STRONG):
+        for B in (1024, 2048):
+            k = L.lorenz_keysetup(b"pw-lengths", mode=mode, block_size=B)
+            prm = ref.params(mode=mode, block_size=B)
+            for n in [0, 1, 15, 1023, 1024, 1025, 2047, 2048, 2049, 10 ** 6, 1 << 30]:
+                assert k.num_blocks(n) == ref.num_blocks(prm, n)
+                assert k.ct_len(n) == ref.ct_len(prm, n)
+                assert L.lorenz_pt_len(k, k.ct_len(n)) == n
+            for bad in [0, 15]:
+                with pytest.raises(L.LorenzError) as e:
+                    L.lorenz_pt_len(k, bad)
+                assert e.value.status == L.E_LENGTH
+    k = L.lorenz_keysetup(b"pw-lengths", mode=L.FAST)
+    with pytest.raises(L.LorenzError):
+        L.lorenz_pt_len(k, 1041)
+
+
+def test_device_calls_reject_bad_ranges_before_launch(L):
+    """Argument errors are returned before any launch (works without a GPU)."""
+    k = L.lorenz_keysetup(b"password", mode=L.FAST)
+    tag = (C.c_uint8 * 16)()
+    lib = L.lib()
+    # b1 > nb
+    assert lib.lorenz_encrypt(C.byref(k.raw), 4096, 0, 9, 16, 4096 + 16 * 64, tag, None) == L.E_ARG
+    # misaligned pointer
+    assert lib.lorenz_encrypt(C.byref(k.raw), 4096, 0, 4, 17, 1 << 20, tag, None) == L.E_ARG
+    # overlapping buffers
+    assert lib.lorenz_encrypt(C.byref(k.raw), 4096, 0, 4, 1 << 20, (1 << 20) + 1024, tag, None) == L.E_ARG
+    # invalid key
+    bad = L.lorenz_key()
+    assert lib.lorenz_encrypt(C.byref(bad), 4096, 0, 4, 16, 1 << 20, tag, None) == L.E_ARG
+    # empty range: a no-op that succeeds without touching the device
+    assert lib.lorenz_encrypt(C.byref(k.raw), 4096, 2, 2, 16, 1 << 20, tag, None) == L.OK
+
+
+def test_product_never_imports_oracle():
+    """The product package shares no code with the oracle and never imports it."""
+    pkg = os.path.join(ROOT, "paper_1201_3114_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in txt and "from oracle" not in txt, f
+                assert "lorenz_ref" not in txt, f

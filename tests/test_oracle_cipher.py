@@ -270,6 +270,17 @@ def test_lock_in_characterisation(ref):
     assert 0.1 <= locked / nb <= 0.6
 
 
+def test_guard_reports_divergence(ref):
+    """Reading Q18: the guard is a status. Forward Euler at the paper's largest step
+    (h = 0.027) is unstable and leaves the box; RK4 at the same step does not."""
+    from paper_1201_3114_b200 import inputs
+    pw, msg = inputs.password(), inputs.message(3 * 1024 + 5, seed=3)
+    with pytest.raises(ref.OracleError) as e:
+        ref.encrypt(pw, msg, _P(ref.FAST, 13, dt_code=3, integ=ref.EULER))
+    assert e.value.status == ref.E_DIVERGENCE
+    ref.encrypt(pw, msg, _P(ref.FAST, 13, dt_code=3, integ=ref.RK4))
+
+
 def test_strong_long_password_is_hashed(ref):
     long_pw = b"x" * 40
     pt = b"hello world"
