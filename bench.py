@@ -48,8 +48,11 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=["c4", "c3"], default="c4")
+    ap.add_argument("--workload", choices=["c4", "c3", "c5"], default="c4")
     ap.add_argument("--n-it", type=int, default=100)
+    ap.add_argument("--integrator", choices=["rk4", "euler"], default="rk4",
+                    help="euler = NEXT-1, the paper's own discretisation (P:178)")
+    ap.add_argument("--c5-trials", type=int, default=128, help="trials per C5 step (3 x 1 MiB streams each)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU time of the oracle sample")
@@ -59,17 +62,23 @@ def parse():
 def workload(name: str):
     if name == "c3":
         return "C3: 64 MiB message, FAST, B=1024, on 1 B200", 64 << 20
+    if name == "c5":
+        return "C5: sensitivity sweep, trials x 3 one-bit-flipped 1 MiB streams per step", 1 << 20
     return "C4: 1 GiB message, FAST, B=1024, block-sharded over N B200", 1 << 30
 
 
-def fp64_ops(n: int, B: int, b0: int, b1: int, n_it: int) -> int:
+OPS_PER_EULER_STEP = 15  # 7 DADD + 8 DMUL
+
+
+def fp64_ops(n: int, B: int, b0: int, b1: int, n_it: int, integrator: str = "rk4") -> int:
     """Algorithmic FP64 ops (DADD+DMUL, no FMA) of blocks [b0,b1): each block advances
     len_b + 15 characters (the last sentinel character is not advanced, Q20)."""
     full = max(0, min(b1, n // B) - b0)
     chars = full * (B + 15)
     for b in range(max(b0, n // B), b1):
         chars += (min(n, (b + 1) * B) - b * B) + 15
-    return chars * (OPS_PER_RK4_STEP * n_it + OPS_PER_CHAR_EXTRA)
+    per_step = OPS_PER_RK4_STEP if integrator == "rk4" else OPS_PER_EULER_STEP
+    return chars * (per_step * n_it + OPS_PER_CHAR_EXTRA)
 
 
 def cores() -> int:
@@ -207,11 +216,88 @@ def cpu_baseline(pw, n_it, B, n, target_s):
                       f"{sec:.1f} s", "cpu": cpu_model()}
 
 
+# ---------------------------------------------------------------- C5 sweep arm
+def run_c5(a):
+    """One step = one batch of a.c5_trials trials (3 x 1 MiB streams each) per rank: the batched
+    encrypt launch plus the statistics kernels. Trials shard across ranks (weak scaling)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1201_3114_b200 import sweep
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    n, B, T = 1 << 20, 1024, a.c5_trials
+    bt = sweep.Batch(rank * T, T, n, a.n_it, B, dev)
+    flush = torch.empty(2 * L2_BYTES, dtype=torch.uint8, device=dev)
+    for _ in range(a.warmup):
+        bt.encrypt()
+        bt.statistics()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    evs = []
+    for _ in range(a.steps):
+        flush.fill_(1)
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        e[0].record()
+        bt.encrypt()
+        e[1].record()
+        bt.statistics()
+        e[2].record()
+        evs.append(e)
+    torch.cuda.synchronize()
+    step_ms = [e[0].elapsed_time(e[2]) for e in evs]
+    enc_ms = [e[0].elapsed_time(e[1]) for e in evs]
+
+    def mx(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+    ms = mx(statistics.mean(step_ms))
+    co, hi, lo = bt.results()
+    pw_bits = co[:, 0, 0] / (8 * bt.ctl)
+    ent = [sweep.entropy_bits(h) for h in hi]
+    value = world * 3 * T * n / (ms / 1e3) / 1e6
+    ops = 3 * T * fp64_ops(n, B, 0, n // B, a.n_it)
+    achieved = ops / (statistics.mean(enc_ms) / 1e3) / 1e12
+    peak = SMS * FP64_LANES_PER_SM * 1965.0 * 1e6 / 1e12
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": round(value, 3), "unit": "MB/s", "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (SplitMix64 messages, printable passwords)",
+            "config": {"workload": workload("c5")[0], "trials_per_rank_step": T, "stream_bytes": n,
+                       "n_it": a.n_it, "block_size": B, "l2": "flushed between timed steps"},
+            "roofline": {"bound": "alu", "achieved": round(achieved, 4), "peak": round(peak, 4),
+                         "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": None,
+                         "kernel": "lz::lorenz_chain_kernel<ENC,RK4> (batch)"},
+            "c5_stats_rank0": {"pw_flip_bit_diff_mean": float(pw_bits.mean()),
+                               "ct_entropy_min": float(min(ent)),
+                               "untouched_blocks_identical": bool((co[:, 2, 1] + co[:, 3, 1]).max() == 0),
+                               "locked_block_fraction": float((lo[:, :, 2] == B - sweep.LOCK_FROM).mean())},
+            "gpu_launches": a.steps * (1 + 2 + 1 + -(-len(bt.lsb_spans) // 65535)),
+            "e2e": None,
+        }), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 # ---------------------------------------------------------------- our arm
 def main():
     a = parse()
     if a.impl == "reference":
         return run_reference(a)
+    if a.workload == "c5":
+        return run_c5(a)
 
     import torch
     import torch.distributed as dist
@@ -230,7 +316,8 @@ def main():
     name, n = workload(a.workload)
     B = 1024
     pw = inputs.password()
-    key = L.lorenz_keysetup(pw, mode=L.FAST, n_it=a.n_it, block_size=B)
+    key = L.lorenz_keysetup(pw, mode=L.FAST, n_it=a.n_it, block_size=B,
+                            integrator=L.EULER if a.integrator == "euler" else L.RK4)
     nb = key.num_blocks(n)
     b0, b1 = D.block_range(nb, rank, world)
     sl = D.slice_of(n, B, b0, b1)
@@ -298,7 +385,7 @@ def main():
     dec_value = n / (dec_sum / a.steps / 1e3) / 1e6
 
     # roofline: the chain kernel's algorithmic FP64 ops per launch / its event time (this rank)
-    ops = fp64_ops(n, B, b0, b1, a.n_it)
+    ops = fp64_ops(n, B, b0, b1, a.n_it, a.integrator)
     kern_s = statistics.mean(enc_ms) / 1e3
     achieved = ops / kern_s / 1e12
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
@@ -344,12 +431,13 @@ def main():
             "warmup": a.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (SplitMix64 message, printable password)",
             "config": {"workload": name, "message_bytes": n, "blocks": nb, "block_size": B, "n_it": a.n_it,
-                       "mode": "FAST", "integrator": "RK4", "dt": 0.01, "parallelism": f"blocks{world}",
+                       "mode": "FAST", "integrator": a.integrator.upper(), "dt": 0.01,
+                       "parallelism": f"blocks{world}",
                        "l2": "flushed between timed steps (2x126 MB write) and inputs > L2"},
             "decrypt": {"value": round(dec_value, 3), "unit": "MB/s", "ms_per_step": round(dec_sum / a.steps, 3)},
             "roofline": {"bound": "alu", "achieved": round(achieved, 4), "peak": round(peak, 4), "unit": "TFLOP/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic,
-                         "kernel": "lz::lorenz_chain_kernel<ENC,RK4>",
+                         "kernel": f"lz::lorenz_chain_kernel<ENC,{a.integrator.upper()}>",
                          "ops_per_launch": ops, "peak_basis": "148 SM x 64 FP64 lanes x sm_max_mhz (DESIGN.md §4)",
                          "hbm_gbs": round((sl.pt_bytes + sl.ct_bytes) / kern_s / 1e9, 3)},
             "fp64_pipe_pct": round(100 * achieved / peak, 2),

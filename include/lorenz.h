@@ -152,6 +152,24 @@ lorenz_status lorenz_encrypt_batch(const lorenz_key* keys, uint32_t S, uint64_t 
                                    const uint8_t* pts, uint8_t* cts, uint8_t* tags,
                                    void* cuda_stream);
 
+/* ---- C5 statistics (§4: histograms/entropy of the ciphertext; "slightly
+ * different passwords"): integer-exact reductions on DEVICE buffers, enqueued on the stream.
+ * `spans` is a HOST array (copied before return). ---- */
+typedef struct {
+  uint64_t a_off; /* byte offset of the span in buffer a */
+  uint64_t b_off; /* byte offset of the span in buffer b (ignored by lorenz_histograms) */
+  uint64_t len;   /* span length in bytes */
+} lorenz_span;
+
+/* For each of `count` spans: out[3i] = differing bits between a[a_off..] and
+ * b[b_off..] over len bytes, out[3i+1] = differing bytes, out[3i+2] = bytes whose least
+ * significant bits are equal. out: DEVICE uint64[3*count], overwritten. */
+lorenz_status lorenz_compare_spans(const uint8_t* a, const uint8_t* b, const lorenz_span* spans,
+                                   uint32_t count, uint64_t* out, void* cuda_stream);
+/* 256-bin byte histogram of each span of a: hist: DEVICE uint64[256*count], overwritten. */
+lorenz_status lorenz_histograms(const uint8_t* a, const lorenz_span* spans, uint32_t count,
+                                uint64_t* hist, void* cuda_stream);
+
 /* ---- end to end from HOST buffers (the user-facing call of a file encryptor):
  * blocks [b0,b1) of an n-byte message; pt_host / ct_host are HOST pointers to the
  * slice starts (same slice convention as the device calls; [0, num_blocks) is the

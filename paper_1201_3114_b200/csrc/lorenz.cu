@@ -13,6 +13,7 @@
 #include "../../include/lorenz.h"
 #include "lorenz_device.cuh"
 #include "sha256.cuh"
+#include "stats.cuh"
 
 namespace {
 
@@ -449,6 +450,52 @@ lorenz_status lorenz_encrypt_batch(const lorenz_key* keys, uint32_t S, uint64_t 
   }
   cudaFreeHost(h_keys);
   return ret;
+}
+
+// ---------------------------------------------------------------- C5 statistics
+}  // extern "C"
+namespace {
+// spans: HOST array; copied to a stream-ordered device buffer. grid.x covers the longest span.
+template <typename Launch>
+lorenz_status span_launch(const lorenz_span* spans, uint32_t count, uint64_t* out, uint64_t out_words,
+                          cudaStream_t st, Launch launch) {
+  if (!cuda_ok(cudaMemsetAsync(out, 0, sizeof(uint64_t) * out_words, st), "memset")) return LORENZ_E_CUDA;
+  uint64_t mx = 0;
+  for (uint32_t i = 0; i < count; ++i) mx = spans[i].len > mx ? spans[i].len : mx;
+  const uint64_t tiles = (mx + lz::kStatTile - 1) / lz::kStatTile;
+  if (!tiles) return LORENZ_OK;
+  lorenz_span* d = nullptr;
+  if (!cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&d), sizeof(lorenz_span) * count, st), "alloc spans"))
+    return LORENZ_E_CUDA;
+  lorenz_status ret = LORENZ_OK;
+  if (!cuda_ok(cudaMemcpyAsync(d, spans, sizeof(lorenz_span) * count, cudaMemcpyHostToDevice, st), "spans H2D"))
+    ret = LORENZ_E_CUDA;
+  if (ret == LORENZ_OK) {
+    launch(dim3((unsigned)tiles, count), d);
+    if (!cuda_ok(cudaGetLastError(), "stats kernel")) ret = LORENZ_E_CUDA;
+  }
+  cudaFreeAsync(d, st);
+  return ret;
+}
+}  // namespace
+extern "C" {
+
+lorenz_status lorenz_compare_spans(const uint8_t* a, const uint8_t* b, const lorenz_span* spans, uint32_t count,
+                                   uint64_t* out, void* stream) {
+  if (!a || !b || !spans || !out || count == 0 || count > 65535) return LORENZ_E_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  return span_launch(spans, count, out, 3ull * count, st, [&](dim3 g, const lorenz_span* d) {
+    lz::compare_spans_kernel<<<g, lz::kStatCta, 0, st>>>(a, b, d, out);
+  });
+}
+
+lorenz_status lorenz_histograms(const uint8_t* a, const lorenz_span* spans, uint32_t count, uint64_t* hist,
+                                void* stream) {
+  if (!a || !spans || !hist || count == 0 || count > 65535) return LORENZ_E_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  return span_launch(spans, count, hist, 256ull * count, st, [&](dim3 g, const lorenz_span* d) {
+    lz::histogram_kernel<<<g, lz::kStatCta, 0, st>>>(a, d, hist);
+  });
 }
 
 // ---------------------------------------------------------------- host-buffer end to end

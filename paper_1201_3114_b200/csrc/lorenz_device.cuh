@@ -43,7 +43,10 @@ struct DevConst {
 enum { OP_ENC = 0, OP_DEC = 1, OP_VERIFY = 2 };
 enum { ST_INTEGRITY = 1, ST_DIVERGENCE = 4 };
 
-constexpr int kCta = 128;              // 4 warps: one per SM sub-partition
+#ifndef LZ_CTA
+#define LZ_CTA 128
+#endif
+constexpr int kCta = LZ_CTA;           // default 4 warps: one per SM sub-partition
 constexpr int kWarps = kCta / 32;
 constexpr int kWin = 64;               // characters per lane per staged window
 constexpr int kRow = kWin + 16;        // smem row stride: per-lane 16-B reads are conflict-free
@@ -338,7 +341,10 @@ __device__ __forceinline__ void st_stream(uint8_t* p, uint4 v) {
 // OP: OP_ENC / OP_DEC / OP_VERIFY. One lane per block; warps are independent
 // (only __syncwarp), so the CTA never waits on its slowest warp.
 template <int OP, int INTEG>
-__global__ void __launch_bounds__(kCta)
+#ifndef LZ_MIN_CTAS
+#define LZ_MIN_CTAS 1
+#endif
+__global__ void __launch_bounds__(kCta, LZ_MIN_CTAS)
     lorenz_chain_kernel(const DevConst C, const DevKey K1, const DevKey* __restrict__ Kb,
                         const uint8_t* __restrict__ in, uint8_t* __restrict__ out,
                         lorenz_result* __restrict__ res, uint8_t* __restrict__ tags_batch,

@@ -15,7 +15,7 @@ import os
 from dataclasses import dataclass
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "csrc", "liblorenz.so")
+LIB_PATH = os.environ.get("LORENZ_LIB") or os.path.join(HERE, "csrc", "liblorenz.so")  # override: tuning runs
 
 OK, E_INTEGRITY, E_ARG, E_PASSWORD, E_LENGTH, E_DIVERGENCE, E_CUDA = range(7)
 STRONG, FAST = 0, 1
@@ -27,7 +27,12 @@ EXPORTS = ["lorenz_abi_version", "lorenz_last_error", "lorenz_status_string", "l
            "lorenz_key_params", "lorenz_num_blocks", "lorenz_ct_len", "lorenz_pt_len",
            "lorenz_encrypt", "lorenz_decrypt", "lorenz_verify", "lorenz_result_init_async",
            "lorenz_encrypt_async", "lorenz_decrypt_async", "lorenz_verify_async",
-           "lorenz_encrypt_batch", "lorenz_encrypt_host", "lorenz_decrypt_host"]
+           "lorenz_encrypt_batch", "lorenz_encrypt_host", "lorenz_decrypt_host",
+           "lorenz_compare_spans", "lorenz_histograms"]
+
+
+class lorenz_span(C.Structure):
+    _fields_ = [("a_off", C.c_uint64), ("b_off", C.c_uint64), ("len", C.c_uint64)]
 
 
 class lorenz_params(C.Structure):
@@ -85,6 +90,8 @@ def lib():
         L.lorenz_decrypt_async.argtypes = [kp, u64, u64, u64, vp, vp, vp, vp, vp]
         L.lorenz_verify_async.argtypes = [kp, u64, u64, u64, vp, vp, vp]
         L.lorenz_encrypt_batch.argtypes = [kp, u32, u64, vp, vp, vp, vp]
+        L.lorenz_compare_spans.argtypes = [vp, vp, C.POINTER(lorenz_span), u32, vp, vp]
+        L.lorenz_histograms.argtypes = [vp, C.POINTER(lorenz_span), u32, vp, vp]
         L.lorenz_encrypt_host.argtypes = [kp, u64, u64, u64, vp, vp, vp, u32]
         L.lorenz_decrypt_host.argtypes = [kp, u64, u64, u64, vp, vp, C.POINTER(C.c_int64), u32]
         for name in EXPORTS:
@@ -216,6 +223,24 @@ def lorenz_encrypt_batch(keys: list[Key], n: int, pts, cts, tags, stream=None):
     arr = (lorenz_key * len(keys))(*[k.raw for k in keys])
     _check(lib().lorenz_encrypt_batch(arr, len(keys), n, _ptr(pts), _ptr(cts), _ptr(tags), _stream(stream)),
            "lorenz_encrypt_batch")
+
+
+def _spans(spans) -> tuple:
+    arr = (lorenz_span * len(spans))(*[lorenz_span(*s) for s in spans])
+    return arr, len(spans)
+
+
+def lorenz_compare_spans(a, b, spans, out, stream=None):
+    """spans: list of (a_off, b_off, len); out: device uint64[3*len(spans)] (bits, bytes, equal-LSB)."""
+    arr, cnt = _spans(spans)
+    _check(lib().lorenz_compare_spans(_ptr(a), _ptr(b), arr, cnt, _ptr(out), _stream(stream)),
+           "lorenz_compare_spans")
+
+
+def lorenz_histograms(a, spans, hist, stream=None):
+    """spans: list of (a_off, _, len); hist: device uint64[256*len(spans)]."""
+    arr, cnt = _spans(spans)
+    _check(lib().lorenz_histograms(_ptr(a), arr, cnt, _ptr(hist), _stream(stream)), "lorenz_histograms")
 
 
 def _host_ptr(buf) -> int | None:

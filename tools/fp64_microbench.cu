@@ -53,7 +53,8 @@ __global__ void lat_kernel(double* out, double a, int n, int mode, unsigned long
 
 // 3-way ILP chain, depth ~6 per "step", 18 ops per step: throughput versus
 // resident warps. Each thread: s = (x,y,z); step: x=x*a+y.. without FMA.
-__global__ void ilp3_kernel(double* out, int steps, double a, double b) {
+__global__ void ilp3_kernel(double* out, int steps, double a, double b, int active = 32) {
+  if ((int)(threadIdx.x & 31) >= active) return;  // partially filled warps (half-warp issue test)
   double x = 1.0 + threadIdx.x * 1e-9, y = 2.0, z = 3.0;
   for (int i = 0; i < steps; ++i) {
     double tx = __dmul_rn(x, a), ty = __dmul_rn(y, a), tz = __dmul_rn(z, a);
@@ -117,6 +118,18 @@ int main() {
     double o = (double)g * 128 * STEPS * 18;
     printf("%s{\"warps_per_sm\": %d, \"ms\": %.3f, \"lane_ops_per_s\": %.4e, \"frac_of_peak\": %.3f}",
            wi ? ", " : "", wps, ms, o / (ms * 1e-3), o / (ms * 1e-3) / rate);
+  }
+  printf("], \"active_lanes_sweep\": [");
+  // same warps (16/SM), fewer active lanes: does a 16-lane warp cost one FP64 pipe cycle or two?
+  int act_list[] = {32, 24, 17, 16, 8, 1};
+  for (int ai = 0; ai < 6; ++ai) {
+    int g = sms * 16 / 4;
+    ilp3_kernel<<<g, 128>>>(d, STEPS, 1.0000001, 1e-12, act_list[ai]); CK(cudaDeviceSynchronize());
+    cudaEventRecord(e0);
+    ilp3_kernel<<<g, 128>>>(d, STEPS, 1.0000001, 1e-12, act_list[ai]);
+    cudaEventRecord(e1); CK(cudaEventSynchronize(e1));
+    float ms; cudaEventElapsedTime(&ms, e0, e1);
+    printf("%s{\"active_lanes\": %d, \"warps_per_sm\": 16, \"ms\": %.3f}", ai ? ", " : "", act_list[ai], ms);
   }
   printf("]}\n");
   return 0;
