@@ -226,11 +226,12 @@ def run_c5(a):
     from paper_1201_3114_b200 import sweep
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    dist_on = world > 1 or "LOCAL_RANK" in os.environ  # torchrun: NCCL even at N = 1
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    if dist_on:
         dist.init_process_group("nccl", device_id=dev)
     n, B, T = 1 << 20, 1024, a.c5_trials
     bt = sweep.Batch(rank * T, T, n, a.n_it, B, dev)
@@ -239,7 +240,7 @@ def run_c5(a):
         bt.encrypt()
         bt.statistics()
     torch.cuda.synchronize()
-    if world > 1:
+    if dist_on:
         dist.barrier()
     evs = []
     for _ in range(a.steps):
@@ -256,7 +257,7 @@ def run_c5(a):
     enc_ms = [e[0].elapsed_time(e[1]) for e in evs]
 
     def mx(x):
-        if world == 1:
+        if not dist_on:
             return x
         t = torch.tensor([x], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -286,7 +287,7 @@ def run_c5(a):
             "gpu_launches": a.steps * (1 + 2 + 1 + -(-len(bt.lsb_spans) // 65535)),
             "e2e": None,
         }), flush=True)
-    if world > 1:
+    if dist_on:
         dist.barrier()
         dist.destroy_process_group()
 
@@ -307,11 +308,12 @@ def main():
     from paper_1201_3114_b200 import lorenz as L
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    dist_on = world > 1 or "LOCAL_RANK" in os.environ  # torchrun: NCCL even at N = 1
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    if dist_on:
         dist.init_process_group("nccl", device_id=dev)
     name, n = workload(a.workload)
     B = 1024
@@ -330,17 +332,17 @@ def main():
     stream = torch.cuda.current_stream()
 
     def barrier():
-        if world > 1:
+        if dist_on:
             dist.barrier()
         torch.cuda.synchronize()
 
     def step_encrypt():
         tag = eng.encrypt(b0, b1, pt, ct)
-        return D.xor_combine(tag) if world > 1 else tag
+        return D.xor_combine(tag) if dist_on else tag
 
     def step_decrypt():
         eng.decrypt(b0, b1, ct, back)
-        return D.min_combine(eng.first_bad()) if world > 1 else eng.first_bad()
+        return D.min_combine(eng.first_bad()) if dist_on else eng.first_bad()
 
     def timed(fn, K):
         """K steps; L2 flushed (write > L2) between steps, outside the events."""
@@ -371,7 +373,7 @@ def main():
     ok = fb == D.NO_BAD and torch.equal(back, pt)
 
     def max_over_ranks(x: float) -> float:
-        if world == 1:
+        if not dist_on:
             return x
         t = torch.tensor([x], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -394,8 +396,8 @@ def main():
     peak = SMS * FP64_LANES_PER_SM * sm_max * 1e6 / 1e12
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_chain_kernel.json")
-    if os.path.exists(tpath):
-        try:
+    if os.path.exists(tpath) and a.workload == "c4" and a.integrator == "rk4" and a.n_it == 100:
+        try:  # from the committed ncu --set full capture of this exact launch configuration
             traffic = json.load(open(tpath)).get("dram_bytes_per_launch_c4_rank_of", {}).get(str(world))
         except (ValueError, OSError):
             traffic = None
@@ -412,7 +414,7 @@ def main():
             barrier()
             t0 = time.perf_counter()
             t = L.lorenz_encrypt_host(key, n, b0, b1, pt_h, ct_h)
-            if world > 1:
+            if dist_on:
                 t_dev.copy_(torch.frombuffer(bytearray(t), dtype=torch.uint8))
                 D.xor_combine(t_dev).cpu()
             times.append(time.perf_counter() - t0)
@@ -449,7 +451,7 @@ def main():
         if cpu:
             out["cpu_baseline"] = cpu
         print(json.dumps(out), flush=True)
-    if world > 1:
+    if dist_on:
         dist.barrier()
         dist.destroy_process_group()
 

@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "../../include/lorenz.h"
 #include "lorenz_device.cuh"
@@ -414,9 +415,7 @@ lorenz_status lorenz_encrypt_batch(const lorenz_key* keys, uint32_t S, uint64_t 
   if (overlap(pts, n * S, cts, ctl * S)) return LORENZ_E_ARG;
   cudaStream_t st = (cudaStream_t)stream;
   lz::DevKey* d_keys = nullptr;
-  lz::DevKey* h_keys = nullptr;
-  if (!cuda_ok(cudaMallocHost(reinterpret_cast<void**>(&h_keys), sizeof(lz::DevKey) * S), "cudaMallocHost"))
-    return LORENZ_E_CUDA;
+  std::vector<lz::DevKey> h_keys(S);  // pageable: the H2D below is staged before it returns
   for (uint32_t s = 0; s < S; ++s) h_keys[s] = make_devkey(impl(&keys[s]));
   lorenz_status ret = LORENZ_OK;
   lorenz_result* d_res = nullptr;
@@ -424,7 +423,8 @@ lorenz_status lorenz_encrypt_batch(const lorenz_key* keys, uint32_t S, uint64_t 
     if (!cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&d_keys), sizeof(lz::DevKey) * S, st), "alloc keys")) {
       ret = LORENZ_E_CUDA; break;
     }
-    if (!cuda_ok(cudaMemcpyAsync(d_keys, h_keys, sizeof(lz::DevKey) * S, cudaMemcpyHostToDevice, st), "keys H2D") ||
+    if (!cuda_ok(cudaMemcpyAsync(d_keys, h_keys.data(), sizeof(lz::DevKey) * S, cudaMemcpyHostToDevice, st),
+                 "keys H2D") ||
         !cuda_ok(cudaMemsetAsync(tags, 0, 16ull * S, st), "tags memset")) {
       ret = LORENZ_E_CUDA; break;
     }
@@ -448,7 +448,6 @@ lorenz_status lorenz_encrypt_batch(const lorenz_key* keys, uint32_t S, uint64_t 
   } else {
     cudaStreamSynchronize(st);
   }
-  cudaFreeHost(h_keys);
   return ret;
 }
 
@@ -501,9 +500,11 @@ lorenz_status lorenz_histograms(const uint8_t* a, const lorenz_span* spans, uint
 // ---------------------------------------------------------------- host-buffer end to end
 namespace {
 struct HostPipe {
-  static constexpr int kStreams = 3;
-  cudaStream_t st[kStreams] = {nullptr, nullptr, nullptr};
-  cudaEvent_t ev[kStreams] = {nullptr, nullptr, nullptr};
+  // one stream per chunk (up to 8): a chunk's kernel starts when its own H2D lands and
+  // the chunks' grids run concurrently, so small chunks never serialise behind each other
+  static constexpr int kStreams = 8;
+  cudaStream_t st[kStreams] = {};
+  cudaEvent_t ev[kStreams] = {};
   bool init() {
     static bool pool_set = false;
     if (!pool_set) {  // keep freed stream-ordered memory cached across calls

@@ -226,20 +226,22 @@ def lorenz_encrypt_batch(keys: list[Key], n: int, pts, cts, tags, stream=None):
 
 
 def _spans(spans) -> tuple:
-    arr = (lorenz_span * len(spans))(*[lorenz_span(*s) for s in spans])
-    return arr, len(spans)
+    """spans: (count, 3) uint64 numpy array (same layout as lorenz_span) or a list of triples."""
+    import numpy as np
+    arr = np.ascontiguousarray(np.asarray(spans, dtype=np.uint64).reshape(-1, 3))
+    return arr.ctypes.data_as(C.POINTER(lorenz_span)), arr.shape[0], arr
 
 
 def lorenz_compare_spans(a, b, spans, out, stream=None):
     """spans: list of (a_off, b_off, len); out: device uint64[3*len(spans)] (bits, bytes, equal-LSB)."""
-    arr, cnt = _spans(spans)
+    arr, cnt, _keep = _spans(spans)
     _check(lib().lorenz_compare_spans(_ptr(a), _ptr(b), arr, cnt, _ptr(out), _stream(stream)),
            "lorenz_compare_spans")
 
 
 def lorenz_histograms(a, spans, hist, stream=None):
     """spans: list of (a_off, _, len); hist: device uint64[256*len(spans)]."""
-    arr, cnt = _spans(spans)
+    arr, cnt, _keep = _spans(spans)
     _check(lib().lorenz_histograms(_ptr(a), arr, cnt, _ptr(hist), _stream(stream)), "lorenz_histograms")
 
 

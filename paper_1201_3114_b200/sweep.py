@@ -80,11 +80,13 @@ class Batch:
             self.spans.append((base + blk + j + 1, ptf_o + blk + j + 1, (B + 16) - j - 1))
             self.spans.append((base, ptf_o, blk))
             self.spans.append((base + blk + B + 16, ptf_o + blk + B + 16, ctl - blk - (B + 16)))
-        self.hist_spans = [(3 * i * ctl, 0, ctl) for i in range(T)]
+        self.spans = np.array(self.spans, dtype=np.uint64)
+        self.hist_spans = np.array([(3 * i * ctl, 0, ctl) for i in range(T)], dtype=np.uint64)
         # LSB equality of base ciphertext vs plaintext, bytes [LOCK_FROM, B) of every block
         self.nb = nb = n // B
-        self.lsb_spans = [(3 * i * ctl + b * (B + 16) + LOCK_FROM, 3 * i * n + b * B + LOCK_FROM, B - LOCK_FROM)
-                          for i in range(T) for b in range(nb)]
+        ii, bb = np.meshgrid(np.arange(T, dtype=np.uint64), np.arange(nb, dtype=np.uint64), indexing="ij")
+        self.lsb_spans = np.stack([3 * ii * ctl + bb * (B + 16) + LOCK_FROM, 3 * ii * n + bb * B + LOCK_FROM,
+                                   np.full_like(ii, B - LOCK_FROM)], axis=-1).reshape(-1, 3)
         self.cmp_out = torch.empty(3 * len(self.spans), dtype=torch.int64, device=dev)
         self.hist = torch.empty(256 * T, dtype=torch.int64, device=dev)
         self.lsb = torch.empty(3 * len(self.lsb_spans), dtype=torch.int64, device=dev)
