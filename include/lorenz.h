@@ -55,7 +55,9 @@ typedef enum {
   LORENZ_E_PASSWORD = 3,   /* password shorter than 3 bytes (Q17)                                 */
   LORENZ_E_LENGTH = 4,     /* ciphertext length inconsistent with the block size                 */
   LORENZ_E_DIVERGENCE = 5, /* guard: non-finite or |x|,|y|>100, z outside [-50,150] (Q18)                */
-  LORENZ_E_CUDA = 6        /* a CUDA runtime error; see lorenz_last_error()                              */
+  LORENZ_E_CUDA = 6,       /* a CUDA runtime error; see lorenz_last_error()                              */
+  LORENZ_E_IO = 7,         /* file open/read/write error (file calls); mirrors SPEC exit code 3  */
+  LORENZ_E_FORMAT = 8      /* bad envelope magic / version / field                                */
 } lorenz_status;
 
 typedef enum { LORENZ_STRONG = 0, LORENZ_FAST = 1 } lorenz_mode;           /* P:446-448 §5 */
@@ -185,6 +187,35 @@ lorenz_status lorenz_encrypt_host(const lorenz_key* k, uint64_t n, uint64_t b0, 
 lorenz_status lorenz_decrypt_host(const lorenz_key* k, uint64_t n, uint64_t b0, uint64_t b1,
                                   const uint8_t* ct_host, uint8_t* pt_host,
                                   int64_t* first_bad_block, uint32_t n_chunks);
+
+/* ---- envelope + streaming file path (NEXT-2; SPEC envelope S:344-390) ----
+ * File = 24-byte header || ciphertext (the concatenation of the blocks' body || tag).
+ * Header (little-endian): "LZX1" | u8 version=1 | u8 mode | u8 flags (bits 0-1: integrator,
+ * an extension; SPEC reserves the byte as 0 = RK4 here) | u8 dt_code | u32 n_it |
+ * u32 chunk_size (= block size B; 0 in STRONG mode) | u64 payload_len (plaintext bytes). */
+#define LORENZ_ENVELOPE_BYTES 24
+
+/* Header of an n-byte message encrypted under k. */
+lorenz_status lorenz_envelope_write(const lorenz_key* k, uint64_t n, uint8_t hdr[LORENZ_ENVELOPE_BYTES]);
+/* Parse a header: params (for lorenz_keysetup with the password), payload length n and the
+ * ciphertext length that must follow. LORENZ_E_LENGTH if len < 24; LORENZ_E_FORMAT for a
+ * bad magic / version / mode / field combination. */
+lorenz_status lorenz_envelope_read(const uint8_t* hdr, size_t len, lorenz_params* p, uint64_t* n,
+                                   uint64_t* ct_len);
+
+/* Encrypt the file at in_path into the envelope file out_path (HOST paths). The file is
+ * streamed through the GPU in block-aligned chunks of about chunk_bytes (0 -> 256 MiB),
+ * three chunks in flight (read -> H2D -> kernel -> D2H -> write), so files larger than
+ * HBM work. The output is written to out_path + ".partial" and renamed on success.
+ * tag_xor (nullable) receives the message digest. Uses the current CUDA device. */
+lorenz_status lorenz_encrypt_file(const char* in_path, const char* out_path, const uint8_t* pw,
+                                  size_t pw_len, const lorenz_params* p, uint64_t chunk_bytes,
+                                  uint8_t tag_xor[16]);
+/* Decrypt an envelope file. The params come from the header. On LORENZ_E_INTEGRITY no
+ * output file is left behind (nothing unauthenticated is released) and *first_bad_block
+ * (nullable) holds the first failing block; LORENZ_E_LENGTH for a truncated body. */
+lorenz_status lorenz_decrypt_file(const char* in_path, const char* out_path, const uint8_t* pw,
+                                  size_t pw_len, uint64_t chunk_bytes, int64_t* first_bad_block);
 
 #ifdef __cplusplus
 }

@@ -19,7 +19,7 @@ LIB_PATH = os.path.join(_HERE, "liblorenz_ref.so")
 
 OK, E_INTEGRITY, E_ARG, E_PASSWORD, E_LENGTH, E_DIVERGENCE = 0, 1, 2, 3, 4, 5
 STRONG, FAST = 0, 1
-RK4, EULER = 0, 1
+RK4, EULER, RK4_FMA = 0, 1, 2
 SENTINEL = b"LORENZCHAOS-MAC1"
 
 
@@ -81,6 +81,7 @@ def lib():
         L.lorenz_ref_rhs.argtypes = [dp, dp]
         L.lorenz_ref_rk4_step.argtypes = [dp, C.c_double]
         L.lorenz_ref_euler_step.argtypes = [dp, C.c_double]
+        L.lorenz_ref_rk4fma_step.argtypes = [dp, C.c_double]
         L.lorenz_ref_iterate.argtypes = [dp, C.c_uint32, C.c_uint32, C.c_uint64]
         L.lorenz_ref_dt.argtypes = [C.c_uint32]
         L.lorenz_ref_dt.restype = C.c_double
@@ -190,6 +191,12 @@ def rhs(s):
 def rk4_step(s, h):
     a = (C.c_double * 3)(*s)
     lib().lorenz_ref_rk4_step(a, h)
+    return tuple(a)
+
+
+def rk4fma_step(s, h):
+    a = (C.c_double * 3)(*s)
+    lib().lorenz_ref_rk4fma_step(a, h)
     return tuple(a)
 
 

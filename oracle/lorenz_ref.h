@@ -34,13 +34,14 @@ extern "C" {
 #define LREF_FAST 1
 #define LREF_RK4 0
 #define LREF_EULER 1
+#define LREF_RK4_FMA 2 /* NEXT-3 */
 
 typedef struct {
   uint32_t mode;       /* LREF_STRONG / LREF_FAST                                   */
   uint32_t n_it;       /* iterations per character; 0 -> 3000 / 100      */
   uint32_t dt_code;    /* 0:0.01 1:0.005 2:0.02 3:0.027 (P:187 range)        */
   uint32_t block_size; /* FAST block size B (bytes); 0 -> 1024                       */
-  uint32_t integrator; /* LREF_RK4 (north star) / LREF_EULER (NEXT-1)         */
+  uint32_t integrator; /* LREF_RK4 (north star) / LREF_EULER (NEXT-1) / LREF_RK4_FMA (NEXT-3) */
 } lref_params;
 
 /* Everything derived from one stream password (§3.1). */
@@ -74,6 +75,7 @@ int lorenz_ref_decode(int c, int ksum);
 void lorenz_ref_rhs(const double s[3], double f[3]);
 void lorenz_ref_rk4_step(double s[3], double h);
 void lorenz_ref_euler_step(double s[3], double h);
+void lorenz_ref_rk4fma_step(double s[3], double h);
 void lorenz_ref_iterate(double s[3], uint32_t dt_code, uint32_t integrator, uint64_t n);
 double lorenz_ref_dt(uint32_t dt_code);
 int lorenz_ref_normalize_password(const uint8_t* pw, size_t n, uint8_t out[23], size_t* n_out);

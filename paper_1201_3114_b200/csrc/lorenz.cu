@@ -178,6 +178,10 @@ lorenz_status alloc_result(lorenz_result** d_res, cudaStream_t st) {
 
 }  // namespace
 
+namespace lz {
+void set_last_error(const std::string& s) { g_err = s; }  // shared with lorenz_io.cu
+}  // namespace lz
+
 // ======================================================================== C ABI
 extern "C" {
 
@@ -194,6 +198,8 @@ const char* lorenz_status_string(lorenz_status s) {
     case LORENZ_E_LENGTH: return "ciphertext length inconsistent with the block size";
     case LORENZ_E_DIVERGENCE: return "trajectory left the guard box";
     case LORENZ_E_CUDA: return "CUDA runtime error";
+    case LORENZ_E_IO: return "file I/O error";
+    case LORENZ_E_FORMAT: return "malformed envelope header";
   }
   return "unknown status";
 }

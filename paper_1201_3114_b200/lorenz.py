@@ -28,7 +28,10 @@ EXPORTS = ["lorenz_abi_version", "lorenz_last_error", "lorenz_status_string", "l
            "lorenz_encrypt", "lorenz_decrypt", "lorenz_verify", "lorenz_result_init_async",
            "lorenz_encrypt_async", "lorenz_decrypt_async", "lorenz_verify_async",
            "lorenz_encrypt_batch", "lorenz_encrypt_host", "lorenz_decrypt_host",
-           "lorenz_compare_spans", "lorenz_histograms"]
+           "lorenz_compare_spans", "lorenz_histograms", "lorenz_envelope_write", "lorenz_envelope_read",
+           "lorenz_encrypt_file", "lorenz_decrypt_file"]
+E_IO, E_FORMAT = 7, 8
+ENVELOPE_BYTES = 24
 
 
 class lorenz_span(C.Structure):
@@ -92,6 +95,12 @@ def lib():
         L.lorenz_encrypt_batch.argtypes = [kp, u32, u64, vp, vp, vp, vp]
         L.lorenz_compare_spans.argtypes = [vp, vp, C.POINTER(lorenz_span), u32, vp, vp]
         L.lorenz_histograms.argtypes = [vp, C.POINTER(lorenz_span), u32, vp, vp]
+        L.lorenz_envelope_write.argtypes = [kp, u64, vp]
+        L.lorenz_envelope_read.argtypes = [C.c_char_p, sz, C.POINTER(lorenz_params), C.POINTER(u64),
+                                           C.POINTER(u64)]
+        L.lorenz_encrypt_file.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, sz, C.POINTER(lorenz_params),
+                                          u64, vp]
+        L.lorenz_decrypt_file.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, sz, u64, C.POINTER(C.c_int64)]
         L.lorenz_encrypt_host.argtypes = [kp, u64, u64, u64, vp, vp, vp, u32]
         L.lorenz_decrypt_host.argtypes = [kp, u64, u64, u64, vp, vp, C.POINTER(C.c_int64), u32]
         for name in EXPORTS:
@@ -243,6 +252,39 @@ def lorenz_histograms(a, spans, hist, stream=None):
     """spans: list of (a_off, _, len); hist: device uint64[256*len(spans)]."""
     arr, cnt, _keep = _spans(spans)
     _check(lib().lorenz_histograms(_ptr(a), arr, cnt, _ptr(hist), _stream(stream)), "lorenz_histograms")
+
+
+def lorenz_envelope_write(key: Key, n: int) -> bytes:
+    hdr = (C.c_uint8 * ENVELOPE_BYTES)()
+    _check(lib().lorenz_envelope_write(C.byref(key.raw), n, hdr), "lorenz_envelope_write")
+    return bytes(hdr)
+
+
+def lorenz_envelope_read(hdr: bytes):
+    """Returns (params, payload_len, ct_len)."""
+    p, n, ctl = lorenz_params(), C.c_uint64(), C.c_uint64()
+    _check(lib().lorenz_envelope_read(bytes(hdr), len(hdr), C.byref(p), C.byref(n), C.byref(ctl)),
+           "lorenz_envelope_read")
+    return p, n.value, ctl.value
+
+
+def lorenz_encrypt_file(in_path: str, out_path: str, pw: bytes, mode: int = FAST, n_it: int = 0,
+                        dt_code: int = 0, block_size: int = 0, integrator: int = RK4, chunk_bytes: int = 0) -> bytes:
+    p = lorenz_params(mode, n_it, dt_code, block_size, integrator)
+    tag = (C.c_uint8 * 16)()
+    _check(lib().lorenz_encrypt_file(os.fsencode(in_path), os.fsencode(out_path), bytes(pw), len(pw), C.byref(p),
+                                     chunk_bytes, tag), "lorenz_encrypt_file")
+    return bytes(tag)
+
+
+def lorenz_decrypt_file(in_path: str, out_path: str, pw: bytes, chunk_bytes: int = 0):
+    """Returns (status, first_bad_block); E_INTEGRITY leaves no output file. Other errors raise."""
+    fb = C.c_int64(-1)
+    st = lib().lorenz_decrypt_file(os.fsencode(in_path), os.fsencode(out_path), bytes(pw), len(pw), chunk_bytes,
+                                   C.byref(fb))
+    if st not in (OK, E_INTEGRITY):
+        raise LorenzError(st, "lorenz_decrypt_file")
+    return st, fb.value
 
 
 def _host_ptr(buf) -> int | None:

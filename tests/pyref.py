@@ -71,13 +71,32 @@ def euler(s, h):
     return [s[c] + d[c] * h for c in range(3)]
 
 
+def fma(a, b, c):
+    """Correctly rounded a*b + c, computed exactly with fractions (Python 3.12 has no math.fma)."""
+    from fractions import Fraction
+    return float(Fraction(a) * Fraction(b) + Fraction(c))
+
+
+def f_fma(x, y, z):
+    return 10.0 * (y - x), fma(-x, z, fma(28.0, x, -y)), fma(x, y, -((8.0 / 3.0) * z))
+
+
+def rk4fma(s, h):
+    h2, h6 = h * 0.5, h / 6.0
+    k1 = f_fma(*s)
+    k2 = f_fma(*[fma(h2, k1[c], s[c]) for c in range(3)])
+    k3 = f_fma(*[fma(h2, k2[c], s[c]) for c in range(3)])
+    k4 = f_fma(*[fma(h, k3[c], s[c]) for c in range(3)])
+    return [fma(h6, fma(2.0, k3[c], fma(2.0, k2[c], k1[c])) + k4[c], s[c]) for c in range(3)]
+
+
 def Rnu(alpha, omega):
     return (int(abs(alpha) * 1e13) >> (8 * omega)) & 0xFF
 
 
 def run_stream(km, data: bytes, n_it: int, dt_code=0, decrypt=False, integrator="rk4"):
     h = DTS[dt_code]
-    step = rk4 if integrator == "rk4" else euler
+    step = {"rk4": rk4, "euler": euler, "rk4fma": rk4fma}[integrator]
     r = list(km["r0"])
     mu, om = list(km["mu"]), list(km["omega"])
     k = [km["k"][0], km["k"][1], km["k3c"]]
