@@ -50,8 +50,8 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=["c4", "c3", "c5"], default="c4")
     ap.add_argument("--n-it", type=int, default=100)
-    ap.add_argument("--integrator", choices=["rk4", "euler"], default="rk4",
-                    help="euler = NEXT-1, the paper's own discretisation (P:178)")
+    ap.add_argument("--integrator", choices=["rk4", "euler", "rk4fma"], default="rk4",
+                    help="euler = NEXT-1, the paper's own discretisation (P:178); rk4fma = NEXT-3")
     ap.add_argument("--c5-trials", type=int, default=128, help="trials per C5 step (3 x 1 MiB streams each)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -67,7 +67,9 @@ def workload(name: str):
     return "C4: 1 GiB message, FAST, B=1024, block-sharded over N B200", 1 << 30
 
 
-OPS_PER_EULER_STEP = 15  # 7 DADD + 8 DMUL
+OPS_PER_EULER_STEP = 15   # 7 DADD + 8 DMUL
+OPS_PER_RK4FMA_STEP = 45  # 7 DADD + 8 DMUL + 30 DFMA pipe operations (= 75 flops, FMA = 2)
+STEP_OPS = {"rk4": OPS_PER_RK4_STEP, "euler": OPS_PER_EULER_STEP, "rk4fma": OPS_PER_RK4FMA_STEP}
 
 
 def fp64_ops(n: int, B: int, b0: int, b1: int, n_it: int, integrator: str = "rk4") -> int:
@@ -77,8 +79,7 @@ def fp64_ops(n: int, B: int, b0: int, b1: int, n_it: int, integrator: str = "rk4
     chars = full * (B + 15)
     for b in range(max(b0, n // B), b1):
         chars += (min(n, (b + 1) * B) - b * B) + 15
-    per_step = OPS_PER_RK4_STEP if integrator == "rk4" else OPS_PER_EULER_STEP
-    return chars * (per_step * n_it + OPS_PER_CHAR_EXTRA)
+    return chars * (STEP_OPS[integrator] * n_it + OPS_PER_CHAR_EXTRA)
 
 
 def cores() -> int:
@@ -319,7 +320,7 @@ def main():
     B = 1024
     pw = inputs.password()
     key = L.lorenz_keysetup(pw, mode=L.FAST, n_it=a.n_it, block_size=B,
-                            integrator=L.EULER if a.integrator == "euler" else L.RK4)
+                            integrator={"rk4": L.RK4, "euler": L.EULER, "rk4fma": L.RK4_FMA}[a.integrator])
     nb = key.num_blocks(n)
     b0, b1 = D.block_range(nb, rank, world)
     sl = D.slice_of(n, B, b0, b1)

@@ -61,7 +61,9 @@ typedef enum {
 } lorenz_status;
 
 typedef enum { LORENZ_STRONG = 0, LORENZ_FAST = 1 } lorenz_mode;           /* P:446-448 §5 */
-typedef enum { LORENZ_RK4 = 0, LORENZ_EULER = 1 } lorenz_integrator;       /* Q1 */
+/* Q1; LORENZ_RK4_FMA (NEXT-3) is RK4 with fused multiply-adds at fixed sites
+ * (DESIGN.md §2b): also IEEE-deterministic, but a different cipher definition. */
+typedef enum { LORENZ_RK4 = 0, LORENZ_EULER = 1, LORENZ_RK4_FMA = 2 } lorenz_integrator;
 
 typedef struct {
   uint32_t mode;       /* lorenz_mode                                                             */

@@ -133,6 +133,9 @@ cudaError_t launch_chain(const lz::DevConst& C, const lz::DevKey& K, const lz::D
   if (grid == 0) return cudaSuccess;
   if (integrator == LORENZ_EULER)
     lz::lorenz_chain_kernel<OP, LORENZ_EULER><<<(unsigned)grid, lz::kCta, 0, st>>>(C, K, Kb, in, out, res, tags, block_ok);
+  else if (integrator == LORENZ_RK4_FMA)
+    lz::lorenz_chain_kernel<OP, LORENZ_RK4_FMA><<<(unsigned)grid, lz::kCta, 0, st>>>(C, K, Kb, in, out, res, tags,
+                                                                                     block_ok);
   else
     lz::lorenz_chain_kernel<OP, LORENZ_RK4><<<(unsigned)grid, lz::kCta, 0, st>>>(C, K, Kb, in, out, res, tags, block_ok);
   return cudaGetLastError();
@@ -207,7 +210,7 @@ const char* lorenz_status_string(lorenz_status s) {
 lorenz_status lorenz_keysetup(const uint8_t* pw, size_t pw_len, const lorenz_params* p, lorenz_key* out) {
   if (!out || (!pw && pw_len)) return LORENZ_E_ARG;
   lorenz_params prm = p ? *p : lorenz_params{LORENZ_FAST, 0, 0, 0, LORENZ_RK4};
-  if (prm.mode > 1 || prm.dt_code > 3 || prm.integrator > 1) return LORENZ_E_ARG;
+  if (prm.mode > 1 || prm.dt_code > 3 || prm.integrator > 2) return LORENZ_E_ARG;
   if (prm.n_it == 0) prm.n_it = prm.mode == LORENZ_FAST ? 100u : 3000u;
   if (prm.mode == LORENZ_FAST) {
     if (prm.block_size == 0) prm.block_size = 1024;

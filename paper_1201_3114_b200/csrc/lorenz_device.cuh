@@ -279,6 +279,29 @@ __device__ __forceinline__ void integrate(double& x, double& y, double& z, const
       x = dadd(x, dmul(h6, sx));
       y = dadd(y, dmul(h6, sy));
       z = dadd(z, dmul(h6, sz));
+    } else if (INTEG == LORENZ_RK4_FMA) {
+      // NEXT-3: same RK4, fused multiply-adds at fixed sites; 45 pipe ops
+      const double k1x = dmul(S, dsub(y, x));
+      const double k1y = __fma_rn(-x, z, __fma_rn(R, x, -y));
+      const double k1z = __fma_rn(x, y, -dmul(Bt, z));
+      const double ax = __fma_rn(h2, k1x, x), ay = __fma_rn(h2, k1y, y), az = __fma_rn(h2, k1z, z);
+      const double k2x = dmul(S, dsub(ay, ax));
+      const double k2y = __fma_rn(-ax, az, __fma_rn(R, ax, -ay));
+      const double k2z = __fma_rn(ax, ay, -dmul(Bt, az));
+      const double bx = __fma_rn(h2, k2x, x), by = __fma_rn(h2, k2y, y), bz = __fma_rn(h2, k2z, z);
+      const double k3x = dmul(S, dsub(by, bx));
+      const double k3y = __fma_rn(-bx, bz, __fma_rn(R, bx, -by));
+      const double k3z = __fma_rn(bx, by, -dmul(Bt, bz));
+      const double cx = __fma_rn(h, k3x, x), cy = __fma_rn(h, k3y, y), cz = __fma_rn(h, k3z, z);
+      const double k4x = dmul(S, dsub(cy, cx));
+      const double k4y = __fma_rn(-cx, cz, __fma_rn(R, cx, -cy));
+      const double k4z = __fma_rn(cx, cy, -dmul(Bt, cz));
+      const double sx = dadd(__fma_rn(2.0, k3x, __fma_rn(2.0, k2x, k1x)), k4x);
+      const double sy = dadd(__fma_rn(2.0, k3y, __fma_rn(2.0, k2y, k1y)), k4y);
+      const double sz = dadd(__fma_rn(2.0, k3z, __fma_rn(2.0, k2z, k1z)), k4z);
+      x = __fma_rn(h6, sx, x);
+      y = __fma_rn(h6, sy, y);
+      z = __fma_rn(h6, sz, z);
     } else {
       const double fx = dmul(S, dsub(y, x));
       const double fy = dsub(dsub(dmul(R, x), y), dmul(x, z));

@@ -164,7 +164,7 @@ lorenz_status lorenz_envelope_read(const uint8_t* hdr, size_t len, lorenz_params
   if (std::memcmp(hdr, "LZX1", 4) != 0 || hdr[4] != 1) return LORENZ_E_FORMAT;
   const uint32_t mode = hdr[5], flags = hdr[6], dt = hdr[7];
   const uint32_t n_it = (uint32_t)get_le(hdr + 8, 4), chunk = (uint32_t)get_le(hdr + 12, 4);
-  if (mode > 1 || flags > 1 || dt > 3 || n_it == 0) return LORENZ_E_FORMAT;
+  if (mode > 1 || flags > 2 || dt > 3 || n_it == 0) return LORENZ_E_FORMAT;
   if (mode == LORENZ_FAST && (chunk < 1024 || chunk % 16)) return LORENZ_E_FORMAT;
   if (mode == LORENZ_STRONG && chunk != 0) return LORENZ_E_FORMAT;
   p->mode = mode;

@@ -19,7 +19,7 @@ LIB_PATH = os.environ.get("LORENZ_LIB") or os.path.join(HERE, "csrc", "liblorenz
 
 OK, E_INTEGRITY, E_ARG, E_PASSWORD, E_LENGTH, E_DIVERGENCE, E_CUDA = range(7)
 STRONG, FAST = 0, 1
-RK4, EULER = 0, 1
+RK4, EULER, RK4_FMA = 0, 1, 2
 TAG_BYTES = 16
 KEY_BYTES = 384
 

@@ -47,7 +47,7 @@ def test_keysetup_deterministic_and_validated(L):
     with pytest.raises(L.LorenzError) as e:
         L.lorenz_keysetup(b"ab")
     assert e.value.status == L.E_PASSWORD
-    for bad in (dict(block_size=1000), dict(block_size=1032), dict(dt_code=4), dict(integrator=2),
+    for bad in (dict(block_size=1000), dict(block_size=1032), dict(dt_code=4), dict(integrator=3),
                 dict(mode=2)):
         with pytest.raises(L.LorenzError) as e:
             L.lorenz_keysetup(b"password", **bad)

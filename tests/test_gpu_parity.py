@@ -144,6 +144,23 @@ def test_dt_codes_and_integrators(dt_code, integrator):
     check_full(pw, msg, **kw)
 
 
+@pytest.mark.parametrize("n,mode,dt_code", [(0, L.FAST, 0), (5 * 1024 + 77, L.FAST, 0), (3000, L.FAST, 3),
+                                            (2000, L.STRONG, 1), (40 * 1024, L.FAST, 2)])
+def test_rk4_fma_variant(n, mode, dt_code):
+    """NEXT-3: the FMA-formulated RK4 (__fma_rn at the oracle's fma() sites) is bit-exact."""
+    check_full(inputs.password(seed=n), inputs.message(n, seed=n + 5), mode=mode, n_it=17, dt_code=dt_code,
+               integrator=L.RK4_FMA)
+
+
+def test_rk4_fma_full_size_sampled():
+    pw = inputs.password()
+    n = 256 << 20
+    msg = inputs.message(n)
+    key = L.lorenz_keysetup(pw, mode=L.FAST, integrator=L.RK4_FMA)
+    ct, tag = gpu_encrypt(key, msg)
+    _sampled_parity(pw, msg, key, ct, tag, 24, seed=45)
+
+
 @pytest.mark.parametrize("B", [1040, 4096, 1 << 20])
 def test_block_sizes(B):
     check_full(inputs.password(), inputs.message(3 * B // 2 + 3), mode=L.FAST, n_it=3, block_size=B)

@@ -50,7 +50,7 @@ def loop_stats(ins):
             tgt = int(m.group(1), 16)
             if tgt < addr:
                 ops = collections.Counter(o.split(".")[0] for a, o, _ in ins if tgt <= a <= addr)
-                fp = ops["DADD"] + ops["DMUL"]
+                fp = ops["DADD"] + ops["DMUL"] + ops["DFMA"]
                 score = fp / max(1, sum(ops.values())) if fp >= 10 else 0.0  # densest FP64 loop
                 if best is None or score > best[0]:
                     best = (score, tgt, addr, addr - tgt, ops)
@@ -70,7 +70,8 @@ def main():
         if best:
             lops = best[4]
             rep["hot_loop"] = {"instructions": sum(lops.values()), "DADD": lops["DADD"], "DMUL": lops["DMUL"],
-                               "DFMA": lops["DFMA"], "other": sum(lops.values()) - lops["DADD"] - lops["DMUL"]}
+                               "DFMA": lops["DFMA"],
+                               "other": sum(lops.values()) - lops["DADD"] - lops["DMUL"] - lops["DFMA"]}
         report[name] = rep
     print(json.dumps(report, indent=1))
 
