@@ -99,9 +99,32 @@ __device__ __forceinline__ double g_divisor(uint32_t L) {
   return v;
 }
 
-// floor(|alpha| * 10^13) of the rounded product (Eq.8, Q8, Q9)
+// floor(|alpha| * 10^13) of the rounded product (Eq.8, Q8, Q9). The product is one DMUL;
+// the floor is taken from its bit pattern on the integer pipes (equal to F2I.U64.TRUNC for
+// every product below 2^64; inside the guard box the product is < 2^51, Q7).
 __device__ __forceinline__ uint64_t quantise(double alpha) {
-  return __double2ull_rz(dmul(fabs(alpha), 1e13));
+  const uint64_t bits = (uint64_t)__double_as_longlong(dmul(fabs(alpha), 1e13));
+  const int e = (int)(bits >> 52) - 1023;  // unbiased exponent (sign bit is clear)
+  const uint64_t mant = (bits & 0xFFFFFFFFFFFFFULL) | (1ULL << 52);
+  if (e < 0) return 0;
+  if (e <= 52) return mant >> (52 - e);
+  return e < 64 ? mant << (e - 52) : ~0ULL;  // only outside the guard box (divergence)
+}
+
+// x mod k for x < 1024, 1 <= k <= 6, with inv = ceil(2^16 / k): one multiply instead of
+// a division (floor(x/k) = (x inv) >> 16 since x (inv - 2^16/k) / 2^16 < 1/64 < 1/k).
+__device__ __forceinline__ uint32_t small_mod(uint32_t x, uint32_t k, uint32_t inv) {
+  return x - k * ((x * inv) >> 16);
+}
+
+// Guard box of Q18 on the integer pipes: |x| <= 100, |y| <= 100, -50 <= z <= 150, all
+// finite (NaN / inf bit patterns compare above every finite bound).
+__device__ __forceinline__ bool in_guard_box(double x, double y, double z) {
+  constexpr uint64_t kAbs = 0x7FFFFFFFFFFFFFFFULL;
+  constexpr uint64_t k100 = 0x4059000000000000ULL, k150 = 0x4062C00000000000ULL, k50 = 0x4049000000000000ULL;
+  const uint64_t bx = (uint64_t)__double_as_longlong(x) & kAbs, by = (uint64_t)__double_as_longlong(y) & kAbs;
+  const uint64_t rz = (uint64_t)__double_as_longlong(z), bz = rz & kAbs;
+  return (bx <= k100) & (by <= k100) & (bz <= ((rz >> 63) ? k50 : k150));
 }
 
 __device__ __forceinline__ uint32_t rbyte(uint64_t m, uint32_t omega) {
@@ -116,6 +139,7 @@ struct Chain {
   uint32_t mu1, mu2, mu3;
   uint32_t om1, om2, om3;  // Eq.7
   uint32_t k1, k2, k3;     // k1,k2 and k3 of Step 3
+  uint32_t ik1, ik2, ik3;  // ceil(2^16 / k) for small_mod
 };
 
 // Key schedule of one stream password. FAST derives the block password
@@ -232,6 +256,9 @@ __device__ __forceinline__ void key_schedule(const DevKey& K, bool fast, uint32_
   ch.k1 = k1i;
   ch.k2 = k2i;
   ch.k3 = 1 + (hk & 0xFF) % 6;
+  ch.ik1 = (65535 + ch.k1) / ch.k1;
+  ch.ik2 = (65535 + ch.k2) / ch.k2;
+  ch.ik3 = (65535 + ch.k3) / ch.k3;
   ch.om1 = (uint32_t)(ho1 % k1i);
   ch.om2 = (uint32_t)(ho2 % k2i);
   ch.om3 = (uint32_t)(ho3 % k3i);
@@ -316,15 +343,16 @@ __device__ __forceinline__ void integrate(double& x, double& y, double& z, const
 // Steps 2-3 after the character's plaintext byte p is known (Q13).
 // Returns false if the guard of Q18 fails.
 template <int INTEG>
-__device__ __forceinline__ bool advance(Chain& ch, uint32_t p, const DevConst& C) {
-  // Step 2: Theta = P_i / 10^{3+Omega_3} (correctly rounded, Q19) added to r[mu_3]
-  const double theta = __ddiv_rn(__uint2double_rn(p), pow10_theta(3 + ch.om3));
+__device__ __forceinline__ bool advance(Chain& ch, uint32_t p, const DevConst& C, const double* theta_tab) {
+  // Step 2: Theta = P_i / 10^{3+Omega_3} (correctly rounded, Q19; from the per-CTA table of
+  // __ddiv_rn quotients) added to r[mu_3]
+  const double theta = theta_tab[ch.om3 * 256 + p];
   const double t = dadd(sel3(ch.mu3, ch.x, ch.y, ch.z), theta);
   ch.x = ch.mu3 == 0 ? t : ch.x;
   ch.y = ch.mu3 == 1 ? t : ch.y;
   ch.z = ch.mu3 == 2 ? t : ch.z;
   integrate<INTEG>(ch.x, ch.y, ch.z, C);
-  const bool ok = (fabs(ch.x) <= 100.0) & (fabs(ch.y) <= 100.0) & (ch.z >= -50.0) & (ch.z <= 150.0);
+  const bool ok = in_guard_box(ch.x, ch.y, ch.z);
   // Step 3: alpha_i = r[mu_i]; R_i = R(alpha_i, Omega_i); mu, Omega += R_i; r += a'
   const uint64_t m1 = quantise(sel3(ch.mu1, ch.x, ch.y, ch.z));
   const uint64_t m2 = quantise(sel3(ch.mu2, ch.x, ch.y, ch.z));
@@ -333,9 +361,9 @@ __device__ __forceinline__ bool advance(Chain& ch, uint32_t p, const DevConst& C
   ch.mu1 = (ch.mu1 + R1) % 3;
   ch.mu2 = (ch.mu2 + R2) % 3;
   ch.mu3 = (ch.mu3 + R3) % 3;
-  ch.om1 = (ch.om1 + R1) % ch.k1;
-  ch.om2 = (ch.om2 + R2) % ch.k2;
-  ch.om3 = (ch.om3 + R3) % ch.k3;
+  ch.om1 = small_mod(ch.om1 + R1, ch.k1, ch.ik1);
+  ch.om2 = small_mod(ch.om2 + R2, ch.k2, ch.ik2);
+  ch.om3 = small_mod(ch.om3 + R3, ch.k3, ch.ik3);
   ch.m1 = m1;
   ch.m2 = m2;
   ch.x = dadd(ch.x, ch.apx);
@@ -373,8 +401,12 @@ __global__ void __launch_bounds__(kCta, LZ_MIN_CTAS)
                         lorenz_result* __restrict__ res, uint8_t* __restrict__ tags_batch,
                         uint8_t* __restrict__ block_ok) {
   __shared__ __align__(16) uint8_t stage[kWarps * 32 * kRow];
+  __shared__ double theta_tab[6 * 256];  // RN(p / 10^{3+e}), e = Omega_3 in [0,6), p a byte
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint8_t* wst = stage + warp * 32 * kRow;
+  for (uint32_t i = threadIdx.x; i < 6 * 256; i += kCta)
+    theta_tab[i] = __ddiv_rn(__uint2double_rn(i & 255), pow10_theta(3 + (i >> 8)));
+  __syncthreads();  // the only CTA-wide barrier; warps run independently afterwards
   const uint64_t g = (uint64_t)blockIdx.x * kCta + threadIdx.x;
   const bool active = g < C.lanes;
 
@@ -464,7 +496,7 @@ __global__ void __launch_bounds__(kCta, LZ_MIN_CTAS)
           tlo = (tlo >> 8) | (thi << 56);
           thi = (thi >> 8) | ((uint64_t)cbyte << 56);
           if (j + 1 == total) break;  // the last character is not advanced (Q20)
-          guard_ok &= advance<INTEG>(ch, p, C);
+          guard_ok &= advance<INTEG>(ch, p, C, theta_tab);
         }
         if (cnt < 16) {  // left-align a partial chunk
           const uint32_t sh = 8 * (16 - cnt);
