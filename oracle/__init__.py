@@ -23,16 +23,19 @@ RK4, EULER, RK4_FMA = 0, 1, 2
 SENTINEL = b"LORENZCHAOS-MAC1"
 
 
+V_LITERAL, V_CYCLIC, V_DISTINCT_K = 1, 2, 4  # NEXT-4 Step-3 reading variants
+
+
 class Params(C.Structure):
     _fields_ = [("mode", C.c_uint32), ("n_it", C.c_uint32), ("dt_code", C.c_uint32),
-                ("block_size", C.c_uint32), ("integrator", C.c_uint32)]
+                ("block_size", C.c_uint32), ("integrator", C.c_uint32), ("variant", C.c_uint32)]
 
 
 class KeyMaterial(C.Structure):
     _fields_ = [("a", C.c_uint64 * 3), ("L", C.c_int), ("d", C.c_int),
                 ("ap", C.c_double * 3), ("lam", C.c_double * 3), ("r0", C.c_double * 3),
                 ("mu", C.c_int * 3), ("k", C.c_int * 3), ("k3chain", C.c_int),
-                ("omega", C.c_int * 3), ("alpha", C.c_double * 3)]
+                ("omega", C.c_int * 3), ("alpha", C.c_double * 3), ("hom", C.c_uint64 * 3)]
 
     def as_dict(self):
         return {"a": tuple(self.a), "L": self.L, "d": self.d, "ap": tuple(self.ap),
@@ -88,6 +91,7 @@ def lib():
         L.lorenz_ref_normalize_password.argtypes = [C.c_char_p, C.c_size_t, u8p, C.POINTER(C.c_size_t)]
         L.lorenz_ref_subpassword.argtypes = [C.c_char_p, C.c_size_t, C.c_uint32, u8p]
         L.lorenz_ref_keymaterial.argtypes = [C.c_char_p, C.c_size_t, C.POINTER(KeyMaterial)]
+        L.lorenz_ref_apply_variant.argtypes = [C.POINTER(KeyMaterial), C.c_uint32]
         L.lorenz_ref_encrypt_stream.argtypes = [C.POINTER(KeyMaterial), C.POINTER(Params), C.c_void_p,
                                                 C.c_size_t, C.c_void_p, C.c_void_p]
         L.lorenz_ref_decrypt_stream.argtypes = [C.POINTER(KeyMaterial), C.POINTER(Params), C.c_void_p,
@@ -114,8 +118,8 @@ class OracleError(RuntimeError):
         self.status = status
 
 
-def params(mode=FAST, n_it=0, dt_code=0, block_size=0, integrator=RK4) -> Params:
-    return Params(mode, n_it, dt_code, block_size, integrator)
+def params(mode=FAST, n_it=0, dt_code=0, block_size=0, integrator=RK4, variant=0) -> Params:
+    return Params(mode, n_it, dt_code, block_size, integrator, variant)
 
 
 # ---------------------------------------------------------------- components
@@ -231,11 +235,12 @@ def subpassword(pw: bytes, b: int) -> bytes:
     return bytes(out)
 
 
-def keymaterial(pw_norm: bytes) -> KeyMaterial:
+def keymaterial(pw_norm: bytes, variant: int = 0) -> KeyMaterial:
     km = KeyMaterial()
     st = lib().lorenz_ref_keymaterial(pw_norm, len(pw_norm), C.byref(km))
     if st:
         raise OracleError(st)
+    lib().lorenz_ref_apply_variant(C.byref(km), variant)
     return km
 
 

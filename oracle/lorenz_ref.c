@@ -171,8 +171,8 @@ void lorenz_ref_mu(const uint64_t a[3], int mu[3]) {
  * k3chain = 1 + H[3] mod 6 (reading Q12).
  * Omega_i = hash(i a) mod k_i (Eq.7): BE64 prefix of
  * SHA-256(BE64(i a1) ‖ BE64(i a2) ‖ BE64(i a3)), products mod 2^64 (Q11).   */
-void lorenz_ref_k_omega(const uint8_t* pw, size_t n, const uint64_t a[3], int k[3],
-                        int* k3chain, int omega[3]) {
+static void k_omega_hashes(const uint8_t* pw, size_t n, const uint64_t a[3], int k[3],
+                           int* k3chain, int omega[3], uint64_t hom[3]) {
   uint8_t H[32];
   lorenz_ref_sha256(pw, n, H);
   for (int i = 0; i < 3; ++i) k[i] = 3 + (H[i] % 2);
@@ -181,8 +181,15 @@ void lorenz_ref_k_omega(const uint8_t* pw, size_t n, const uint64_t a[3], int k[
     uint8_t msg[24], dig[32];
     for (int j = 0; j < 3; ++j) put_be64(msg + 8 * j, (uint64_t)i * a[j]);
     lorenz_ref_sha256(msg, sizeof msg, dig);
-    omega[i - 1] = (int)(be64(dig) % (uint64_t)k[i - 1]);
+    hom[i - 1] = be64(dig);
+    omega[i - 1] = (int)(hom[i - 1] % (uint64_t)k[i - 1]);
   }
+}
+
+void lorenz_ref_k_omega(const uint8_t* pw, size_t n, const uint64_t a[3], int k[3],
+                        int* k3chain, int omega[3]) {
+  uint64_t hom[3];
+  k_omega_hashes(pw, n, a, k, k3chain, omega, hom);
 }
 
 /* Passwords longer than 23 bytes are replaced by SHA-256(pi)[0:18]; shorter
@@ -229,9 +236,18 @@ int lorenz_ref_keymaterial(const uint8_t* pw_norm, size_t n, lref_km* km) {
   lorenz_ref_lambda(km->a, km->lam);
   for (int i = 0; i < 3; ++i) km->r0[i] = km->ap[i] + km->lam[i];
   lorenz_ref_mu(km->a, km->mu);
-  lorenz_ref_k_omega(pw_norm, n, km->a, km->k, &km->k3chain, km->omega);
+  k_omega_hashes(pw_norm, n, km->a, km->k, &km->k3chain, km->omega, km->hom);
   for (int i = 0; i < 3; ++i) km->alpha[i] = km->r0[km->mu[i]];
   return LREF_OK;
+}
+
+/* NEXT-4 variant "distinct k": k2 = 7 - k1, so k1 != k2 (both stay in
+ * the paper's range 2 < k <= 4) and Omega0_2 = hash(2a) mod the new k2.       */
+void lorenz_ref_apply_variant(lref_km* km, uint32_t variant) {
+  if (variant & LREF_V_DISTINCT_K) {
+    km->k[1] = 7 - km->k[0];
+    km->omega[1] = (int)(km->hom[1] % (uint64_t)km->k[1]);
+  }
 }
 
 /* ======================================================================== */
@@ -398,14 +414,34 @@ static int chain_advance(chain_t* ch, int p, const lref_params* prm) {
   /* the trajectory: n_it iterations of the map */
   lorenz_ref_iterate(ch->r, prm->dt_code, prm->integrator, prm->n_it);
   if (!guard_ok(ch->r)) return LREF_E_DIVERGENCE;
-  /* Step 3, order of reading Q13: alpha_i = r[mu_i] (Eq.6 with the
-   * old mu); R_i = R(alpha_i, Omega_i) with the old Omega; mu_i = (mu_i + R_i)
-   * mod 3; Omega_i = (Omega_i + R_i) mod k_i; then r = r + a'.              */
   int R[3];
-  for (int i = 0; i < 3; ++i) ch->alpha[i] = ch->r[ch->mu[i]];
-  for (int i = 0; i < 3; ++i) R[i] = lorenz_ref_R(ch->alpha[i], ch->omega[i]);
-  for (int i = 0; i < 3; ++i) ch->mu[i] = (ch->mu[i] + R[i]) % 3;
-  for (int i = 0; i < 3; ++i) ch->omega[i] = (ch->omega[i] + R[i]) % ch->k[i];
+  if ((prm->variant & LREF_V_ORDER_MASK) == LREF_V_LITERAL) {
+    /* NEXT-4 literal textual order of P:320-322: mu_i' = [mu_i + R(alpha_i, Omega_i)] mod 3
+     * with the alpha of the previous character; then "alpha given by Eq.6" from the new mu;
+     * then Omega_i = [Omega_i' + R(alpha_{[(i+2) mod 3]+1}, Omega_i')] mod k_i, where the
+     * printed permutation is the identity for 1-based i.                        */
+    for (int i = 0; i < 3; ++i) R[i] = lorenz_ref_R(ch->alpha[i], ch->omega[i]);
+    for (int i = 0; i < 3; ++i) ch->mu[i] = (ch->mu[i] + R[i]) % 3;
+    for (int i = 0; i < 3; ++i) ch->alpha[i] = ch->r[ch->mu[i]];
+    for (int i = 0; i < 3; ++i)
+      ch->omega[i] = (ch->omega[i] + lorenz_ref_R(ch->alpha[i], ch->omega[i])) % ch->k[i];
+  } else {
+    /* Step 3, order of reading Q13: alpha_i = r[mu_i] (Eq.6 with the
+     * old mu); R_i = R(alpha_i, Omega_i) with the old Omega; mu_i = (mu_i + R_i)
+     * mod 3; Omega_i = (Omega_i + R_i) mod k_i.                                */
+    for (int i = 0; i < 3; ++i) ch->alpha[i] = ch->r[ch->mu[i]];
+    for (int i = 0; i < 3; ++i) R[i] = lorenz_ref_R(ch->alpha[i], ch->omega[i]);
+    for (int i = 0; i < 3; ++i) ch->mu[i] = (ch->mu[i] + R[i]) % 3;
+    if ((prm->variant & LREF_V_ORDER_MASK) == LREF_V_CYCLIC) {
+      /* NEXT-4 cyclic reading of the index [(i+2) mod 3]+1: Omega_i takes its byte from
+       * alpha_{i+1} (alpha_1 for i = 3) instead of alpha_i.                         */
+      for (int i = 0; i < 3; ++i)
+        ch->omega[i] = (ch->omega[i] + lorenz_ref_R(ch->alpha[(i + 1) % 3], ch->omega[i])) % ch->k[i];
+    } else {
+      for (int i = 0; i < 3; ++i) ch->omega[i] = (ch->omega[i] + R[i]) % ch->k[i];
+    }
+  }
+  /* r_n = r_n + a' */
   for (int i = 0; i < 3; ++i) ch->r[i] = ch->r[i] + ch->ap[i];
   return LREF_OK;
 }
@@ -492,6 +528,7 @@ int lorenz_ref_pt_len(const lref_params* prm_in, uint64_t ct_len, uint64_t* n_ou
 
 static int check_params(const lref_params* prm) {
   if (prm->mode > 1 || prm->integrator > 2 || prm->dt_code > 3) return LREF_E_ARG;
+  if ((prm->variant & LREF_V_ORDER_MASK) == 3 || prm->variant > 7) return LREF_E_ARG;
   if (prm->mode == LREF_FAST && (prm->block_size < 1024 || prm->block_size % 16)) return LREF_E_ARG;
   return LREF_OK;
 }
@@ -499,16 +536,20 @@ static int check_params(const lref_params* prm) {
 /* key material of global block b */
 static int block_km(const uint8_t* pw, size_t pw_len, const lref_params* prm, uint64_t b,
                     lref_km* km) {
+  int st;
   if (prm->mode == LREF_FAST) {
     uint8_t sub[18];
     lorenz_ref_subpassword(pw, pw_len, (uint32_t)b, sub);
-    return lorenz_ref_keymaterial(sub, 18, km);
+    st = lorenz_ref_keymaterial(sub, 18, km);
+  } else {
+    uint8_t norm[23];
+    size_t nn;
+    st = lorenz_ref_normalize_password(pw, pw_len, norm, &nn);
+    if (st) return st;
+    st = lorenz_ref_keymaterial(norm, nn, km);
   }
-  uint8_t norm[23];
-  size_t nn;
-  int st = lorenz_ref_normalize_password(pw, pw_len, norm, &nn);
-  if (st) return st;
-  return lorenz_ref_keymaterial(norm, nn, km);
+  if (!st) lorenz_ref_apply_variant(km, prm->variant);
+  return st;
 }
 
 typedef struct {

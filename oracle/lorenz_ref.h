@@ -42,7 +42,14 @@ typedef struct {
   uint32_t dt_code;    /* 0:0.01 1:0.005 2:0.02 3:0.027 (P:187 range)        */
   uint32_t block_size; /* FAST block size B (bytes); 0 -> 1024                       */
   uint32_t integrator; /* LREF_RK4 (north star) / LREF_EULER (NEXT-1) / LREF_RK4_FMA (NEXT-3) */
+  uint32_t variant;    /* NEXT-4 Step-3 reading variants; 0 = the adopted reading (Q13)          */
 } lref_params;
+
+/* NEXT-4 variant bits */
+#define LREF_V_ORDER_MASK 3u
+#define LREF_V_LITERAL 1u    /* literal textual order of P:320-322 */
+#define LREF_V_CYCLIC 2u     /* cyclic reading of the index [(i+2) mod 3]+1 */
+#define LREF_V_DISTINCT_K 4u /* k2 = 7 - k1 */
 
 /* Everything derived from one stream password (§3.1). */
 typedef struct {
@@ -57,6 +64,7 @@ typedef struct {
   int k3chain;       /* k3 of Step 3, in [1,6] */
   int omega[3];      /* Omega0 (Eq.7) */
   double alpha[3];   /* alpha0 (Eq.6, n=0) */
+  uint64_t hom[3];   /* BE64 prefixes of hash(i a) (Eq.7) before the mod */
 } lref_km;
 
 /* ---- components (each pinned separately in tests/) ---- */
@@ -81,6 +89,7 @@ double lorenz_ref_dt(uint32_t dt_code);
 int lorenz_ref_normalize_password(const uint8_t* pw, size_t n, uint8_t out[23], size_t* n_out);
 void lorenz_ref_subpassword(const uint8_t* pw, size_t n, uint32_t b, uint8_t out[18]);
 int lorenz_ref_keymaterial(const uint8_t* pw_norm, size_t n, lref_km* km);
+void lorenz_ref_apply_variant(lref_km* km, uint32_t variant);
 
 /* ---- one stream (§3.2 Steps 1-3) ----
  * encrypt: c must hold len+16 bytes (body ‖ encrypted sentinel).

@@ -30,7 +30,7 @@ def pack(pw: bytes):
     return [a1, a2, a3], L
 
 
-def key_material(pw: bytes):
+def key_material(pw: bytes, variant: int = 0):
     a, L = pack(pw)
     d = len(str(2 ** (8 * (L + 1))))          # ceil(log10 2^{8(L+1)})
     ap = [float(ai) / float(10 ** d) for ai in a]
@@ -46,10 +46,13 @@ def key_material(pw: bytes):
     H = hashlib.sha256(pw).digest()
     k = [3 + H[0] % 2, 3 + H[1] % 2, 3 + H[2] % 2]
     k3c = 1 + H[3] % 6
-    om = []
+    hs = []
     for i in (1, 2, 3):
         msg = b"".join(((i * x) % 2 ** 64).to_bytes(8, "big") for x in a)
-        om.append(int.from_bytes(hashlib.sha256(msg).digest()[:8], "big") % k[i - 1])
+        hs.append(int.from_bytes(hashlib.sha256(msg).digest()[:8], "big"))
+    if variant & 4:  # NEXT-4 "distinct k": k2 = 7 - k1
+        k[1] = 7 - k[0]
+    om = [hs[i] % k[i] for i in range(3)]
     return dict(a=a, ap=ap, r0=r0, mu=mu, k=k, k3c=k3c, omega=om)
 
 
@@ -94,7 +97,9 @@ def Rnu(alpha, omega):
     return (int(abs(alpha) * 1e13) >> (8 * omega)) & 0xFF
 
 
-def run_stream(km, data: bytes, n_it: int, dt_code=0, decrypt=False, integrator="rk4"):
+def run_stream(km, data: bytes, n_it: int, dt_code=0, decrypt=False, integrator="rk4", variant=0):
+    """variant bits 0-1 (NEXT-4 Step-3 order): 0 adopted reading, 1 literal text order,
+    2 cyclic index; bit 2 (distinct k) is applied in key_material."""
     h = DTS[dt_code]
     step = {"rk4": rk4, "euler": euler, "rk4fma": rk4fma}[integrator]
     r = list(km["r0"])
@@ -113,10 +118,19 @@ def run_stream(km, data: bytes, n_it: int, dt_code=0, decrypt=False, integrator=
         r[mu[2]] = r[mu[2]] + float(p) / float(10 ** (3 + om[2]))
         for _ in range(n_it):
             r = step(r, h)
-        alpha = [r[mu[i]] for i in range(3)]
-        Rv = [Rnu(alpha[i], om[i]) for i in range(3)]
-        mu = [(mu[i] + Rv[i]) % 3 for i in range(3)]
-        om = [(om[i] + Rv[i]) % k[i] for i in range(3)]
+        order = variant & 3
+        if order == 1:  # mu from the previous alpha, then alpha from the new mu, then Omega
+            mu = [(mu[i] + Rnu(alpha[i], om[i])) % 3 for i in range(3)]
+            alpha = [r[mu[i]] for i in range(3)]
+            om = [(om[i] + Rnu(alpha[i], om[i])) % k[i] for i in range(3)]
+        else:
+            alpha = [r[mu[i]] for i in range(3)]
+            Rv = [Rnu(alpha[i], om[i]) for i in range(3)]
+            mu = [(mu[i] + Rv[i]) % 3 for i in range(3)]
+            if order == 2:
+                om = [(om[i] + Rnu(alpha[(i + 1) % 3], om[i])) % k[i] for i in range(3)]
+            else:
+                om = [(om[i] + Rv[i]) % k[i] for i in range(3)]
         r = [r[i] + km["ap"][i] for i in range(3)]
     return bytes(out)
 
