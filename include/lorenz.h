@@ -46,7 +46,7 @@ extern "C" {
 
 #define LORENZ_TAG_BYTES 16
 #define LORENZ_KEY_BYTES 384
-#define LORENZ_ABI_VERSION 1
+#define LORENZ_ABI_VERSION 2
 
 typedef enum {
   LORENZ_OK = 0,
@@ -71,7 +71,13 @@ typedef struct {
   uint32_t dt_code;    /* step h: 0 -> 0.01, 1 -> 0.005, 2 -> 0.02, 3 -> 0.027 (0 < h <= 0.027) */
   uint32_t block_size; /* FAST block size B: >= 1024 and a multiple of 16; 0 -> 1024. STRONG: ignored */
   uint32_t integrator; /* lorenz_integrator; LORENZ_EULER is the paper's own discretisation  */
+  uint32_t variant;    /* NEXT-4 Step-3 reading: 0 = adopted reading Q13;
+                          bits 0-1: 1 = literal textual order, 2 = cyclic index; bit 2: k2 = 7 - k1   */
 } lorenz_params;
+
+#define LORENZ_V_LITERAL 1u
+#define LORENZ_V_CYCLIC 2u
+#define LORENZ_V_DISTINCT_K 4u
 
 /* Key: POD, caller-owned, trivially copyable, no heap. Holds the params, the exact
  * binary64 bit patterns of sigma, rho, beta, h, h/2, h/6, and the password:

@@ -19,15 +19,16 @@ assert HEADER.size == 24
 
 
 def effective(prm: Params) -> tuple:
-    """(mode, n_it, dt_code, block_size, integrator) with the defaults of S:33 / S:312."""
+    """(mode, n_it, dt_code, block_size, flags) with the defaults of S:33 / S:312; flags =
+    integrator | variant << 2 (0 for the default cipher, as SPEC's reserved byte)."""
     n_it = prm.n_it or (100 if prm.mode == FAST else 3000)
     B = (prm.block_size or 1024) if prm.mode == FAST else 0
-    return prm.mode, n_it, prm.dt_code, B, prm.integrator
+    return prm.mode, n_it, prm.dt_code, B, prm.integrator | (prm.variant << 2)
 
 
 def header(prm: Params, n: int) -> bytes:
-    mode, n_it, dt, B, integ = effective(prm)
-    return HEADER.pack(b"LZX1", 1, mode, integ, dt, n_it, B, n)
+    mode, n_it, dt, B, flags = effective(prm)
+    return HEADER.pack(b"LZX1", 1, mode, flags, dt, n_it, B, n)
 
 
 def parse(hdr: bytes) -> dict:
@@ -36,7 +37,7 @@ def parse(hdr: bytes) -> dict:
     magic, ver, mode, flags, dt, n_it, chunk, n = HEADER.unpack(hdr[:HEADER.size])
     if magic != b"LZX1" or ver != 1 or mode not in (STRONG, FAST):
         raise ValueError("bad magic/version/mode")
-    return dict(mode=mode, integrator=flags, dt_code=dt, n_it=n_it, block_size=chunk, n=n)
+    return dict(mode=mode, integrator=flags & 3, variant=flags >> 2, dt_code=dt, n_it=n_it, block_size=chunk, n=n)
 
 
 def encrypt_file_bytes(pw: bytes, data: bytes, prm: Params) -> bytes:

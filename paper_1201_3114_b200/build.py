@@ -45,7 +45,22 @@ def build(force: bool = False, verbose: bool = False) -> str:
         print(r.stderr)
     with open(os.path.join(CSRC, "ptxas.log"), "w") as f:
         f.write(r.stderr)
+    build_cli()
     return LIB
+
+
+CLI = os.path.join(HERE, "bin", "lorenz")
+
+
+def build_cli() -> str:
+    """The `lorenz` command (csrc/lorenz_cli.cpp) linked against liblorenz.so (rpath $ORIGIN/../csrc)."""
+    os.makedirs(os.path.dirname(CLI), exist_ok=True)
+    cmd = ["g++", "-O2", "-std=c++17", "-Wall", os.path.join(CSRC, "lorenz_cli.cpp"), "-L" + CSRC, "-llorenz",
+           "-Wl,-rpath,$ORIGIN/../csrc", "-o", CLI]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError("g++ (cli) failed:\n" + r.stdout + r.stderr)
+    return CLI
 
 
 if __name__ == "__main__":

@@ -122,6 +122,7 @@ lz::DevConst make_const(const KeyImpl* K, uint64_t n, uint64_t b0, uint64_t lane
   C.nb = nblocks(K, n);
   C.n_it = K->prm.n_it;
   C.fast = K->prm.mode == LORENZ_FAST;
+  C.variant = K->prm.variant;
   return C;
 }
 
@@ -209,8 +210,9 @@ const char* lorenz_status_string(lorenz_status s) {
 
 lorenz_status lorenz_keysetup(const uint8_t* pw, size_t pw_len, const lorenz_params* p, lorenz_key* out) {
   if (!out || (!pw && pw_len)) return LORENZ_E_ARG;
-  lorenz_params prm = p ? *p : lorenz_params{LORENZ_FAST, 0, 0, 0, LORENZ_RK4};
+  lorenz_params prm = p ? *p : lorenz_params{LORENZ_FAST, 0, 0, 0, LORENZ_RK4, 0};
   if (prm.mode > 1 || prm.dt_code > 3 || prm.integrator > 2) return LORENZ_E_ARG;
+  if (prm.variant > 7 || (prm.variant & 3) == 3) return LORENZ_E_ARG;
   if (prm.n_it == 0) prm.n_it = prm.mode == LORENZ_FAST ? 100u : 3000u;
   if (prm.mode == LORENZ_FAST) {
     if (prm.block_size == 0) prm.block_size = 1024;

@@ -37,7 +37,7 @@ struct DevConst {
   uint32_t n_it;                       // map iterations per character
   uint32_t fast;                       // 1: per-block sub-keys
   uint32_t batch;                      // 1: keys from the device array, tags per message
-  uint32_t pad_;
+  uint32_t variant;                    // NEXT-4 Step-3 reading (0 = Q13; see lorenz.h)
 };
 
 enum { OP_ENC = 0, OP_DEC = 1, OP_VERIFY = 2 };
@@ -136,6 +136,7 @@ struct Chain {
   double x, y, z;          // r
   double apx, apy, apz;    // a', added after every character
   uint64_t m1, m2;         // floor(|alpha_1,2| 10^13) feeding Step 1
+  uint64_t m3;             // floor(|alpha_3| 10^13) (used by the literal-order variant)
   uint32_t mu1, mu2, mu3;
   uint32_t om1, om2, om3;  // Eq.7
   uint32_t k1, k2, k3;     // k1,k2 and k3 of Step 3
@@ -145,7 +146,8 @@ struct Chain {
 // Key schedule of one stream password. FAST derives the block password
 // SHA-256(pw || BE32 b)[0:18] from the midstate first (Q16). All hashes run
 // through one in-register compression inside a job loop (small code, no local memory).
-__device__ __forceinline__ void key_schedule(const DevKey& K, bool fast, uint32_t b, Chain& ch) {
+__device__ __forceinline__ void key_schedule(const DevKey& K, bool fast, uint32_t b, uint32_t variant,
+                                             Chain& ch) {
   uint32_t pw[6];
   uint32_t np;
   Sha256State s;
@@ -252,7 +254,9 @@ __device__ __forceinline__ void key_schedule(const DevKey& K, bool fast, uint32_
     }
   }
   // k_i = 3 + H[i-1] mod 2; k3 of Step 3 = 1 + H[3] mod 6 (Q12)
-  const uint32_t k1i = 3 + ((hk >> 24) & 1), k2i = 3 + ((hk >> 16) & 1), k3i = 3 + ((hk >> 8) & 1);
+  const uint32_t k1i = 3 + ((hk >> 24) & 1), k3i = 3 + ((hk >> 8) & 1);
+  // NEXT-4 "distinct k": k2 = 7 - k1
+  const uint32_t k2i = (variant & LORENZ_V_DISTINCT_K) ? 7 - k1i : 3 + ((hk >> 16) & 1);
   ch.k1 = k1i;
   ch.k2 = k2i;
   ch.k3 = 1 + (hk & 0xFF) % 6;
@@ -273,6 +277,7 @@ __device__ __forceinline__ void key_schedule(const DevKey& K, bool fast, uint32_
   ch.z = dadd(ch.apz, lam3);
   ch.m1 = quantise(sel3(ch.mu1, ch.x, ch.y, ch.z));
   ch.m2 = quantise(sel3(ch.mu2, ch.x, ch.y, ch.z));
+  ch.m3 = quantise(sel3(ch.mu3, ch.x, ch.y, ch.z));
 }
 
 // n_it steps of the Lorenz map. RK4 in the canonical order of DESIGN.md §2
@@ -353,19 +358,41 @@ __device__ __forceinline__ bool advance(Chain& ch, uint32_t p, const DevConst& C
   ch.z = ch.mu3 == 2 ? t : ch.z;
   integrate<INTEG>(ch.x, ch.y, ch.z, C);
   const bool ok = in_guard_box(ch.x, ch.y, ch.z);
-  // Step 3: alpha_i = r[mu_i]; R_i = R(alpha_i, Omega_i); mu, Omega += R_i; r += a'
-  const uint64_t m1 = quantise(sel3(ch.mu1, ch.x, ch.y, ch.z));
-  const uint64_t m2 = quantise(sel3(ch.mu2, ch.x, ch.y, ch.z));
-  const uint64_t m3 = quantise(sel3(ch.mu3, ch.x, ch.y, ch.z));
-  const uint32_t R1 = rbyte(m1, ch.om1), R2 = rbyte(m2, ch.om2), R3 = rbyte(m3, ch.om3);
-  ch.mu1 = (ch.mu1 + R1) % 3;
-  ch.mu2 = (ch.mu2 + R2) % 3;
-  ch.mu3 = (ch.mu3 + R3) % 3;
-  ch.om1 = small_mod(ch.om1 + R1, ch.k1, ch.ik1);
-  ch.om2 = small_mod(ch.om2 + R2, ch.k2, ch.ik2);
-  ch.om3 = small_mod(ch.om3 + R3, ch.k3, ch.ik3);
-  ch.m1 = m1;
-  ch.m2 = m2;
+  const uint32_t order = C.variant & 3;  // warp-uniform
+  if (order == LORENZ_V_LITERAL) {
+    // NEXT-4 literal order: mu from the previous alpha, alpha from the new mu, then Omega
+    ch.mu1 = (ch.mu1 + rbyte(ch.m1, ch.om1)) % 3;
+    ch.mu2 = (ch.mu2 + rbyte(ch.m2, ch.om2)) % 3;
+    ch.mu3 = (ch.mu3 + rbyte(ch.m3, ch.om3)) % 3;
+    ch.m1 = quantise(sel3(ch.mu1, ch.x, ch.y, ch.z));
+    ch.m2 = quantise(sel3(ch.mu2, ch.x, ch.y, ch.z));
+    ch.m3 = quantise(sel3(ch.mu3, ch.x, ch.y, ch.z));
+    ch.om1 = small_mod(ch.om1 + rbyte(ch.m1, ch.om1), ch.k1, ch.ik1);
+    ch.om2 = small_mod(ch.om2 + rbyte(ch.m2, ch.om2), ch.k2, ch.ik2);
+    ch.om3 = small_mod(ch.om3 + rbyte(ch.m3, ch.om3), ch.k3, ch.ik3);
+  } else {
+    // Step 3 (Q13): alpha_i = r[mu_i]; R_i = R(alpha_i, Omega_i); mu, Omega += R_i
+    const uint64_t m1 = quantise(sel3(ch.mu1, ch.x, ch.y, ch.z));
+    const uint64_t m2 = quantise(sel3(ch.mu2, ch.x, ch.y, ch.z));
+    const uint64_t m3 = quantise(sel3(ch.mu3, ch.x, ch.y, ch.z));
+    const uint32_t R1 = rbyte(m1, ch.om1), R2 = rbyte(m2, ch.om2), R3 = rbyte(m3, ch.om3);
+    ch.mu1 = (ch.mu1 + R1) % 3;
+    ch.mu2 = (ch.mu2 + R2) % 3;
+    ch.mu3 = (ch.mu3 + R3) % 3;
+    if (order == LORENZ_V_CYCLIC) {  // NEXT-4: Omega_i takes its byte from alpha_{i+1}
+      ch.om1 = small_mod(ch.om1 + rbyte(m2, ch.om1), ch.k1, ch.ik1);
+      ch.om2 = small_mod(ch.om2 + rbyte(m3, ch.om2), ch.k2, ch.ik2);
+      ch.om3 = small_mod(ch.om3 + rbyte(m1, ch.om3), ch.k3, ch.ik3);
+    } else {
+      ch.om1 = small_mod(ch.om1 + R1, ch.k1, ch.ik1);
+      ch.om2 = small_mod(ch.om2 + R2, ch.k2, ch.ik2);
+      ch.om3 = small_mod(ch.om3 + R3, ch.k3, ch.ik3);
+    }
+    ch.m1 = m1;
+    ch.m2 = m2;
+    ch.m3 = m3;
+  }
+  // r_n = r_n + a'
   ch.x = dadd(ch.x, ch.apx);
   ch.y = dadd(ch.y, ch.apy);
   ch.z = dadd(ch.z, ch.apz);
@@ -427,7 +454,7 @@ __global__ void __launch_bounds__(kCta, LZ_MIN_CTAS)
   Chain ch;
   if (active) {
     const DevKey& K = C.batch ? Kb[s] : K1;
-    key_schedule(K, C.fast != 0, (uint32_t)bl, ch);
+    key_schedule(K, C.fast != 0, (uint32_t)bl, C.variant, ch);
   }
 
   bool guard_ok = true, bad = false;

@@ -149,7 +149,7 @@ lorenz_status lorenz_envelope_write(const lorenz_key* k, uint64_t n, uint8_t hdr
   std::memcpy(hdr, "LZX1", 4);
   hdr[4] = 1;
   hdr[5] = (uint8_t)p.mode;
-  hdr[6] = (uint8_t)(p.integrator & 3);
+  hdr[6] = (uint8_t)((p.integrator & 3) | (p.variant << 2));  // 0 for the default cipher (SPEC)
   hdr[7] = (uint8_t)p.dt_code;
   put_le(hdr + 8, p.n_it, 4);
   put_le(hdr + 12, p.mode == LORENZ_FAST ? p.block_size : 0, 4);
@@ -164,14 +164,16 @@ lorenz_status lorenz_envelope_read(const uint8_t* hdr, size_t len, lorenz_params
   if (std::memcmp(hdr, "LZX1", 4) != 0 || hdr[4] != 1) return LORENZ_E_FORMAT;
   const uint32_t mode = hdr[5], flags = hdr[6], dt = hdr[7];
   const uint32_t n_it = (uint32_t)get_le(hdr + 8, 4), chunk = (uint32_t)get_le(hdr + 12, 4);
-  if (mode > 1 || flags > 2 || dt > 3 || n_it == 0) return LORENZ_E_FORMAT;
+  const uint32_t integ = flags & 3, variant = flags >> 2;
+  if (mode > 1 || integ > 2 || variant > 7 || (variant & 3) == 3 || dt > 3 || n_it == 0) return LORENZ_E_FORMAT;
   if (mode == LORENZ_FAST && (chunk < 1024 || chunk % 16)) return LORENZ_E_FORMAT;
   if (mode == LORENZ_STRONG && chunk != 0) return LORENZ_E_FORMAT;
   p->mode = mode;
   p->n_it = n_it;
   p->dt_code = dt;
   p->block_size = chunk;
-  p->integrator = flags;
+  p->integrator = integ;
+  p->variant = variant;
   *n = get_le(hdr + 16, 8);
   if (ct_len) {
     const uint64_t nb = mode == LORENZ_STRONG ? 1 : ((*n + chunk - 1) / chunk ? (*n + chunk - 1) / chunk : 1);

@@ -40,7 +40,10 @@ class lorenz_span(C.Structure):
 
 class lorenz_params(C.Structure):
     _fields_ = [("mode", C.c_uint32), ("n_it", C.c_uint32), ("dt_code", C.c_uint32),
-                ("block_size", C.c_uint32), ("integrator", C.c_uint32)]
+                ("block_size", C.c_uint32), ("integrator", C.c_uint32), ("variant", C.c_uint32)]
+
+
+V_LITERAL, V_CYCLIC, V_DISTINCT_K = 1, 2, 4  # NEXT-4 Step-3 reading variants
 
 
 class lorenz_key(C.Structure):
@@ -159,9 +162,9 @@ class Key:
 
 
 def lorenz_keysetup(pw: bytes, mode: int = FAST, n_it: int = 0, dt_code: int = 0, block_size: int = 0,
-                    integrator: int = RK4) -> Key:
+                    integrator: int = RK4, variant: int = 0) -> Key:
     k = lorenz_key()
-    p = lorenz_params(mode, n_it, dt_code, block_size, integrator)
+    p = lorenz_params(mode, n_it, dt_code, block_size, integrator, variant)
     _check(lib().lorenz_keysetup(bytes(pw), len(pw), C.byref(p), C.byref(k)), "lorenz_keysetup")
     return Key(k)
 
@@ -269,8 +272,9 @@ def lorenz_envelope_read(hdr: bytes):
 
 
 def lorenz_encrypt_file(in_path: str, out_path: str, pw: bytes, mode: int = FAST, n_it: int = 0,
-                        dt_code: int = 0, block_size: int = 0, integrator: int = RK4, chunk_bytes: int = 0) -> bytes:
-    p = lorenz_params(mode, n_it, dt_code, block_size, integrator)
+                        dt_code: int = 0, block_size: int = 0, integrator: int = RK4, chunk_bytes: int = 0,
+                        variant: int = 0) -> bytes:
+    p = lorenz_params(mode, n_it, dt_code, block_size, integrator, variant)
     tag = (C.c_uint8 * 16)()
     _check(lib().lorenz_encrypt_file(os.fsencode(in_path), os.fsencode(out_path), bytes(pw), len(pw), C.byref(p),
                                      chunk_bytes, tag), "lorenz_encrypt_file")

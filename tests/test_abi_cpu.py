@@ -33,7 +33,7 @@ def test_exports_every_declared_symbol(L):
     for s in syms:
         assert hasattr(so, s), s
     assert set(L.EXPORTS) == set(syms)
-    assert L.lib().lorenz_abi_version() == 1
+    assert L.lib().lorenz_abi_version() == 2
 
 
 def test_keysetup_deterministic_and_validated(L):

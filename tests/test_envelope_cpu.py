@@ -19,15 +19,18 @@ def test_header_matches_oracle(L, ref):
     for _ in range(200):
         mode = rng.choice([L.FAST, L.STRONG])
         kw = dict(mode=mode, n_it=rng.choice([0, 1, 100, 3000, 77]), dt_code=rng.randrange(4),
-                  block_size=rng.choice([0, 1024, 1040, 65536]), integrator=rng.randrange(2))
+                  block_size=rng.choice([0, 1024, 1040, 65536]), integrator=rng.randrange(3),
+                  variant=rng.choice([0, 0, 1, 2, 4, 5, 6]))
         key = L.lorenz_keysetup(b"envelope-pw", **kw)
         n = rng.choice([0, 5, 1024, 10 ** 6, 1 << 33])
         hdr = L.lorenz_envelope_write(key, n)
         assert hdr == envelope.header(ref.params(**kw), n)
         p, n2, ctl = L.lorenz_envelope_read(hdr)
         eff = key.params
-        assert (p.mode, p.n_it, p.dt_code, p.block_size, p.integrator) == \
-            (eff.mode, eff.n_it, eff.dt_code, eff.block_size, eff.integrator)
+        assert (p.mode, p.n_it, p.dt_code, p.block_size, p.integrator, p.variant) == \
+            (eff.mode, eff.n_it, eff.dt_code, eff.block_size, eff.integrator, eff.variant)
+        if kw["integrator"] == 0 and kw["variant"] == 0:
+            assert hdr[6] == 0  # SPEC's reserved flags byte for the default cipher
         assert n2 == n and ctl == key.ct_len(n)
         assert envelope.parse(hdr)["n"] == n
 

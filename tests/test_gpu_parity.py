@@ -23,7 +23,7 @@ DEV = torch.device("cuda:0")
 def oparams(key: L.Key):
     p = key.params
     return oracle.params(mode=p.mode, n_it=p.n_it, dt_code=p.dt_code, block_size=p.block_size,
-                         integrator=p.integrator)
+                         integrator=p.integrator, variant=p.variant)
 
 
 def gpu_encrypt(key, msg: np.ndarray):
@@ -150,6 +150,23 @@ def test_rk4_fma_variant(n, mode, dt_code):
     """NEXT-3: the FMA-formulated RK4 (__fma_rn at the oracle's fma() sites) is bit-exact."""
     check_full(inputs.password(seed=n), inputs.message(n, seed=n + 5), mode=mode, n_it=17, dt_code=dt_code,
                integrator=L.RK4_FMA)
+
+
+@pytest.mark.parametrize("variant", [1, 2, 4, 5, 6])
+@pytest.mark.parametrize("mode,n", [(L.FAST, 5 * 1024 + 77), (L.STRONG, 700)])
+def test_step3_variants(variant, mode, n):
+    """NEXT-4: the Step-3 reading variants are bit-exact against the pinned oracle."""
+    check_full(inputs.password(seed=variant), inputs.message(n, seed=variant), mode=mode, n_it=23,
+               variant=variant)
+
+
+def test_step3_variant_full_size_sampled():
+    pw = inputs.password()
+    n = 128 << 20
+    msg = inputs.message(n)
+    key = L.lorenz_keysetup(pw, mode=L.FAST, variant=L.V_CYCLIC | L.V_DISTINCT_K)
+    ct, tag = gpu_encrypt(key, msg)
+    _sampled_parity(pw, msg, key, ct, tag, 24, seed=46)
 
 
 def test_rk4_fma_full_size_sampled():
