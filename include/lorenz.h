@@ -180,6 +180,17 @@ lorenz_status lorenz_compare_spans(const uint8_t* a, const uint8_t* b, const lor
 lorenz_status lorenz_histograms(const uint8_t* a, const lorenz_span* spans, uint32_t count,
                                 uint64_t* hist, void* cuda_stream);
 
+/* ---- NEXT-4 analysis: Fig.1 of the paper, frequency of the integer part and of
+ * the decimal digit pairs 1-2, 3-4, 5-6 of the Lorenz coordinates. `lanes` trajectories start
+ * at ic (DEVICE, lanes x 3 doubles, x y z), run `skip` transient steps, then every coordinate
+ * of the state after each `stride` steps is binned, `samples` times:
+ *   hist[(c*4 + kind)*128 + bin], c = x,y,z; kind 0: bin = trunc(v) + 64 (clamped to 0..127);
+ *   kind k = 1..3: bin = floor(RN(|v| * 10^{2k})) mod 100.
+ * hist: DEVICE uint64[3*4*128], overwritten. Same integrators / dt codes as the cipher. */
+lorenz_status lorenz_digit_histograms(const double* ic, uint64_t lanes, uint32_t skip, uint32_t samples,
+                                      uint32_t stride, uint32_t dt_code, uint32_t integrator,
+                                      uint64_t* hist, void* cuda_stream);
+
 /* ---- end to end from HOST buffers (the user-facing call of a file encryptor):
  * blocks [b0,b1) of an n-byte message; pt_host / ct_host are HOST pointers to the
  * slice starts (same slice convention as the device calls; [0, num_blocks) is the
@@ -212,8 +223,8 @@ lorenz_status lorenz_envelope_read(const uint8_t* hdr, size_t len, lorenz_params
                                    uint64_t* ct_len);
 
 /* Encrypt the file at in_path into the envelope file out_path (HOST paths). The file is
- * streamed through the GPU in block-aligned chunks of about chunk_bytes (0 -> 256 MiB),
- * three chunks in flight (read -> H2D -> kernel -> D2H -> write), so files larger than
+ * streamed through the GPU in block-aligned chunks of about chunk_bytes (0 -> 32 MiB),
+ * four chunks in flight (read -> H2D -> kernel -> D2H -> write), so files larger than
  * HBM work. The output is written to out_path + ".partial" and renamed on success.
  * tag_xor (nullable) receives the message digest. Uses the current CUDA device. */
 lorenz_status lorenz_encrypt_file(const char* in_path, const char* out_path, const uint8_t* pw,

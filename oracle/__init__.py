@@ -103,6 +103,8 @@ def lib():
         L.lorenz_ref_pt_len.argtypes = [C.POINTER(Params), C.c_uint64, u64p]
         L.lorenz_ref_encrypt.argtypes = [C.c_char_p, C.c_size_t, C.POINTER(Params), C.c_uint64, C.c_uint64,
                                          C.c_uint64, C.c_void_p, C.c_void_p, u8p, C.c_int]
+        L.lorenz_ref_digit_hist.argtypes = [C.c_void_p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32,
+                                            C.c_uint32, C.c_uint32, C.c_void_p]
         L.lorenz_ref_encrypt_block.argtypes = [C.c_char_p, C.c_size_t, C.POINTER(Params), C.c_uint64,
                                                C.c_uint64, C.c_void_p, C.c_void_p]
         L.lorenz_ref_decrypt.argtypes = [C.c_char_p, C.c_size_t, C.POINTER(Params), C.c_uint64, C.c_uint64,
@@ -305,6 +307,15 @@ def encrypt(pw: bytes, pt, prm: Params, b0=0, b1=None, threads=0):
     if st:
         raise OracleError(st)
     return ct, bytes(tag)
+
+
+def digit_hist(ic: np.ndarray, skip: int, samples: int, stride: int, dt_code=0, integrator=RK4) -> np.ndarray:
+    """Fig.1 digit histograms of trajectories from ic (lanes x 3 doubles): uint64[3, 4, 128]."""
+    ic = np.ascontiguousarray(ic, dtype=np.float64).reshape(-1, 3)
+    hist = np.zeros((3, 4, 128), dtype=np.uint64)
+    lib().lorenz_ref_digit_hist(ic.ctypes.data, ic.shape[0], skip, samples, stride, dt_code, integrator,
+                                hist.ctypes.data)
+    return hist
 
 
 def encrypt_block(pw: bytes, n: int, b: int, blk_pt, prm: Params) -> np.ndarray:

@@ -640,6 +640,41 @@ int lorenz_ref_encrypt(const uint8_t* pw, size_t pw_len, const lref_params* prm_
   return LREF_OK;
 }
 
+/* ======================================================================== */
+/* NEXT-4 analysis: Fig.1 digit frequencies (§3.1)                 */
+/* ======================================================================== */
+/* "frequency distribution of the integer part as well as the decimal part of the Lorenz's
+ * attractor": (a) integer part, (b) 1st-2nd, (c) 3rd-4th, (d) 5th-6th decimal digits.
+ * Reading: every coordinate v of the state after each `stride` steps,
+ * following `skip` transient steps, of each trajectory; a = |v|;
+ *   kind 0: bin = trunc(v) + 64 (clamped to [0,127]);
+ *   kind k = 1,2,3: bin = floor(RN(a * 10^{2k})) mod 100.
+ * hist[(c*4 + kind)*128 + bin], c = x,y,z; accumulated (not cleared).                  */
+void lorenz_ref_digit_hist(const double* ic, uint64_t lanes, uint32_t skip, uint32_t samples,
+                           uint32_t stride, uint32_t dt_code, uint32_t integrator, uint64_t* hist) {
+  const double scale[4] = {0.0, 100.0, 10000.0, 1000000.0};
+  for (uint64_t l = 0; l < lanes; ++l) {
+    double s[3] = {ic[3 * l], ic[3 * l + 1], ic[3 * l + 2]};
+    lorenz_ref_iterate(s, dt_code, integrator, skip);
+    for (uint32_t t = 0; t < samples; ++t) {
+      lorenz_ref_iterate(s, dt_code, integrator, stride);
+      for (int c = 0; c < 3; ++c) {
+        double v = s[c];
+        long long ip = (long long)v; /* truncation toward zero */
+        long long b0 = ip + 64;
+        if (b0 < 0) b0 = 0;
+        if (b0 > 127) b0 = 127;
+        hist[(c * 4 + 0) * 128 + b0] += 1;
+        double a = fabs(v);
+        for (int k = 1; k <= 3; ++k) {
+          uint64_t m = (uint64_t)(a * scale[k]);
+          hist[(c * 4 + k) * 128 + (m % 100)] += 1;
+        }
+      }
+    }
+  }
+}
+
 /* One global block b of a message of length n, from that block's own bytes:
  * blk_pt = the block's plaintext (len_b bytes), blk_ct receives len_b + 16 bytes. */
 int lorenz_ref_encrypt_block(const uint8_t* pw, size_t pw_len, const lref_params* prm_in, uint64_t n,

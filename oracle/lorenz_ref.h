@@ -110,6 +110,9 @@ int lorenz_ref_pt_len(const lref_params* prm, uint64_t ct_len, uint64_t* n_out);
 int lorenz_ref_encrypt(const uint8_t* pw, size_t pw_len, const lref_params* prm, uint64_t n,
                        uint64_t b0, uint64_t b1, const uint8_t* pt, uint8_t* ct,
                        uint8_t tag_xor[16], int threads);
+/* NEXT-4 analysis: Fig.1 digit histograms; hist: uint64[3*4*128], accumulated. */
+void lorenz_ref_digit_hist(const double* ic, uint64_t lanes, uint32_t skip, uint32_t samples,
+                           uint32_t stride, uint32_t dt_code, uint32_t integrator, uint64_t* hist);
 /* One global block b of a message of length n, from that block's own bytes. */
 int lorenz_ref_encrypt_block(const uint8_t* pw, size_t pw_len, const lref_params* prm, uint64_t n,
                              uint64_t b, const uint8_t* blk_pt, uint8_t* blk_ct);

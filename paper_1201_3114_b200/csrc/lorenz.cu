@@ -13,6 +13,7 @@
 
 #include "../../include/lorenz.h"
 #include "lorenz_device.cuh"
+#include "analysis.cuh"
 #include "sha256.cuh"
 #include "stats.cuh"
 
@@ -460,6 +461,31 @@ lorenz_status lorenz_encrypt_batch(const lorenz_key* keys, uint32_t S, uint64_t 
     cudaStreamSynchronize(st);
   }
   return ret;
+}
+
+// ---------------------------------------------------------------- NEXT-4 analysis (Fig.1)
+lorenz_status lorenz_digit_histograms(const double* ic, uint64_t lanes, uint32_t skip, uint32_t samples,
+                                      uint32_t stride, uint32_t dt_code, uint32_t integrator, uint64_t* hist,
+                                      void* stream) {
+  if (!hist || (lanes && !ic) || dt_code > 3 || integrator > 2 || lanes > (1ULL << 40)) return LORENZ_E_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!cuda_ok(cudaMemsetAsync(hist, 0, sizeof(uint64_t) * lz::kHistBins, st), "memset")) return LORENZ_E_CUDA;
+  if (lanes == 0) return LORENZ_OK;
+  lorenz_key k;  // the constants exactly as a key holds them
+  lorenz_params p{LORENZ_FAST, 1, dt_code, 0, integrator, 0};
+  const uint8_t dummy[3] = {'a', 'b', 'c'};
+  lorenz_status s = lorenz_keysetup(dummy, 3, &p, &k);
+  if (s != LORENZ_OK) return s;
+  const lz::DevConst C = make_const(impl(&k), 0, 0, lanes);
+  const unsigned grid = (unsigned)((lanes + lz::kCta - 1) / lz::kCta);
+  auto* h = reinterpret_cast<unsigned long long*>(hist);
+  if (integrator == LORENZ_EULER)
+    lz::digit_hist_kernel<LORENZ_EULER><<<grid, lz::kCta, 0, st>>>(C, ic, lanes, skip, samples, stride, h);
+  else if (integrator == LORENZ_RK4_FMA)
+    lz::digit_hist_kernel<LORENZ_RK4_FMA><<<grid, lz::kCta, 0, st>>>(C, ic, lanes, skip, samples, stride, h);
+  else
+    lz::digit_hist_kernel<LORENZ_RK4><<<grid, lz::kCta, 0, st>>>(C, ic, lanes, skip, samples, stride, h);
+  return cuda_ok(cudaGetLastError(), "digit_hist") ? LORENZ_OK : LORENZ_E_CUDA;
 }
 
 // ---------------------------------------------------------------- C5 statistics

@@ -55,6 +55,21 @@ def message(n: int, seed: int = SEED_MSG, start: int = 0, out: np.ndarray | None
     return res
 
 
+SEED_IC = 0xF161  # Fig.1 trajectories
+# initial states uniform in the lambda box of P:216 widened by a' <= 1: where r0 lives
+IC_LO = (-15.67, -11.28, 0.090)
+IC_HI = (17.01, 17.01, 63.0)
+
+
+def initial_states(lanes: int, seed: int = SEED_IC) -> np.ndarray:
+    """(lanes, 3) float64: component c of lane l = lo_c + u (hi_c - lo_c), u = 53-bit uniform
+    from SplitMix64(seed XOR (3 l + c))."""
+    idx = np.arange(3 * lanes, dtype=np.uint64) ^ np.uint64(seed)
+    u = (splitmix64(idx) >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
+    lo, hi = np.array(IC_LO * lanes), np.array(IC_HI * lanes)
+    return (lo + u * (hi - lo)).reshape(lanes, 3)
+
+
 def password(seed: int = SEED_PW, length: int = 16) -> bytes:
     return bytes(0x21 + splitmix64(seed ^ k) % 94 for k in range(length))
 

@@ -29,7 +29,7 @@ EXPORTS = ["lorenz_abi_version", "lorenz_last_error", "lorenz_status_string", "l
            "lorenz_encrypt_async", "lorenz_decrypt_async", "lorenz_verify_async",
            "lorenz_encrypt_batch", "lorenz_encrypt_host", "lorenz_decrypt_host",
            "lorenz_compare_spans", "lorenz_histograms", "lorenz_envelope_write", "lorenz_envelope_read",
-           "lorenz_encrypt_file", "lorenz_decrypt_file"]
+           "lorenz_encrypt_file", "lorenz_decrypt_file", "lorenz_digit_histograms"]
 E_IO, E_FORMAT = 7, 8
 ENVELOPE_BYTES = 24
 
@@ -98,6 +98,7 @@ def lib():
         L.lorenz_encrypt_batch.argtypes = [kp, u32, u64, vp, vp, vp, vp]
         L.lorenz_compare_spans.argtypes = [vp, vp, C.POINTER(lorenz_span), u32, vp, vp]
         L.lorenz_histograms.argtypes = [vp, C.POINTER(lorenz_span), u32, vp, vp]
+        L.lorenz_digit_histograms.argtypes = [vp, u64, u32, u32, u32, u32, u32, vp, vp]
         L.lorenz_envelope_write.argtypes = [kp, u64, vp]
         L.lorenz_envelope_read.argtypes = [C.c_char_p, sz, C.POINTER(lorenz_params), C.POINTER(u64),
                                            C.POINTER(u64)]
@@ -255,6 +256,13 @@ def lorenz_histograms(a, spans, hist, stream=None):
     """spans: list of (a_off, _, len); hist: device uint64[256*len(spans)]."""
     arr, cnt, _keep = _spans(spans)
     _check(lib().lorenz_histograms(_ptr(a), arr, cnt, _ptr(hist), _stream(stream)), "lorenz_histograms")
+
+
+def lorenz_digit_histograms(ic, lanes: int, skip: int, samples: int, stride: int, hist, dt_code: int = 0,
+                            integrator: int = RK4, stream=None):
+    """Fig.1 digit histograms (NEXT-4): ic device float64 (lanes x 3), hist device int64[3*4*128]."""
+    _check(lib().lorenz_digit_histograms(_ptr(ic), lanes, skip, samples, stride, dt_code, integrator, _ptr(hist),
+                                         _stream(stream)), "lorenz_digit_histograms")
 
 
 def lorenz_envelope_write(key: Key, n: int) -> bytes:

@@ -21,7 +21,7 @@ from paper_1201_3114_b200 import lorenz as L  # noqa: E402
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--mib", type=int, default=1024)
-    ap.add_argument("--chunk-mib", type=int, default=256)
+    ap.add_argument("--chunk-mib", type=int, default=32)
     ap.add_argument("--dir", default="/dev/shm" if os.path.isdir("/dev/shm") else tempfile.gettempdir())
     ap.add_argument("--reps", type=int, default=2)
     a = ap.parse_args()
