@@ -88,6 +88,10 @@ def test_device_calls_reject_bad_ranges_before_launch(L):
     assert lib.lorenz_encrypt(C.byref(bad), 4096, 0, 4, 16, 1 << 20, tag, None) == L.E_ARG
     # empty range: a no-op that succeeds without touching the device
     assert lib.lorenz_encrypt(C.byref(k.raw), 4096, 2, 2, 16, 1 << 20, tag, None) == L.OK
+    # maximum size: block indices are BE32 in the sub-key (Q16), so nb > 2^32 is refused
+    huge = (1 << 32) * 1024 + 1
+    assert k.num_blocks(huge) == (1 << 32) + 1
+    assert lib.lorenz_encrypt(C.byref(k.raw), huge, 0, 1, 16, 1 << 40, tag, None) == L.E_ARG
 
 
 def test_product_never_imports_oracle():
