@@ -25,9 +25,11 @@ def main():
     ap.add_argument("--mib", type=int, nargs="+", default=[64, 128, 256, 1024])
     ap.add_argument("--n-it", type=int, default=100)
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--integrator", choices=["rk4", "euler", "rk4fma"], default="rk4")
     a = ap.parse_args()
     dev = torch.device("cuda:0")
-    key = L.lorenz_keysetup(inputs.password(), mode=L.FAST, n_it=a.n_it)
+    integ = {"rk4": L.RK4, "euler": L.EULER, "rk4fma": L.RK4_FMA}[a.integrator]
+    key = L.lorenz_keysetup(inputs.password(), mode=L.FAST, n_it=a.n_it, integrator=integ)
     big = max(a.mib) << 20
     msg = torch.from_numpy(inputs.message(big)).to(dev)
     ct = torch.empty(key.ct_len(big), dtype=torch.uint8, device=dev)
@@ -48,8 +50,8 @@ def main():
             torch.cuda.synchronize()
             ts.append(e0.elapsed_time(e1) / 1e3)
         t = min(ts)
-        ops = fp64_ops(n, 1024, 0, nb, a.n_it)
-        print(json.dumps({"tag": a.tag, "mib": mib, "blocks": nb, "ms": round(t * 1e3, 3),
+        ops = fp64_ops(n, 1024, 0, nb, a.n_it, a.integrator)
+        print(json.dumps({"tag": a.tag, "integrator": a.integrator, "mib": mib, "blocks": nb, "ms": round(t * 1e3, 3),
                           "MBps": round(n / t / 1e6, 1), "frac": round(ops / t / peak, 4)}), flush=True)
 
 
