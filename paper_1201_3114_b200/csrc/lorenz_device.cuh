@@ -415,14 +415,20 @@ __device__ __forceinline__ void st_stream(uint8_t* p, uint4 v) {
   __stcs(reinterpret_cast<uint4*>(p), v);
 }
 
+#ifndef LZ_MIN_CTAS
+#define LZ_MIN_CTAS 1
+#endif
+// Resident CTAs per SM (tools/tune.py sweep): RK4 and Euler are at their best with the
+// compiler's register choice (4 CTAs, <= 128 registers); the FMA form gains 2 points
+// (92.7 % -> 94.8 % of the FP64 pipe on C4) from a fifth CTA (<= 102 registers).
+template <int INTEG>
+constexpr int min_ctas() { return INTEG == LORENZ_RK4_FMA ? 5 : LZ_MIN_CTAS; }
+
 // ------------------------------------------------------------------ the kernel
 // OP: OP_ENC / OP_DEC / OP_VERIFY. One lane per block; warps are independent
 // (only __syncwarp), so the CTA never waits on its slowest warp.
 template <int OP, int INTEG>
-#ifndef LZ_MIN_CTAS
-#define LZ_MIN_CTAS 1
-#endif
-__global__ void __launch_bounds__(kCta, LZ_MIN_CTAS)
+__global__ void __launch_bounds__(kCta, min_ctas<INTEG>())
     lorenz_chain_kernel(const DevConst C, const DevKey K1, const DevKey* __restrict__ Kb,
                         const uint8_t* __restrict__ in, uint8_t* __restrict__ out,
                         lorenz_result* __restrict__ res, uint8_t* __restrict__ tags_batch,
