@@ -127,20 +127,50 @@ lz::DevConst make_const(const KeyImpl* K, uint64_t n, uint64_t b0, uint64_t lane
   return C;
 }
 
+int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+  }
+  return n;
+}
+
+// CTA size for a launch of `lanes` chains (16 resident warps per SM either way). The kernel
+// is FP64-pipe bound, so its makespan follows the largest number of warps any SM processes
+// over the launch: 4 * ceil(CTAs/SMs) with 128-thread CTAs, 8 * ceil(CTAs/SMs) with 256.
+// Take the smaller; on a tie 256 measured 0.3-3 % faster (tools/tune.py, 13 sizes from
+// 16 MiB to 1 GiB: the rule picked the faster size at every one).
+int chain_cta(uint64_t lanes, uint32_t integrator) {
+  if (integrator == LORENZ_RK4_FMA) return 128;  // 5 CTAs/SM of 128 (see min_ctas)
+  const uint64_t warps = (lanes + 31) / 32, sms = (uint64_t)sm_count();
+  const uint64_t c128 = (warps + 3) / 4, c256 = (warps + 7) / 8;  // CTAs of 4 / 8 warps
+  const uint64_t l128 = 4 * ((c128 + sms - 1) / sms), l256 = 8 * ((c256 + sms - 1) / sms);
+  return l256 <= l128 ? 256 : 128;
+}
+
+template <int OP, int INTEG, int CTA>
+cudaError_t launch_chain_cta(const lz::DevConst& C, const lz::DevKey& K, const lz::DevKey* Kb, const uint8_t* in,
+                             uint8_t* out, lorenz_result* res, uint8_t* tags, uint8_t* block_ok, cudaStream_t st) {
+  const uint64_t grid = (C.lanes + CTA - 1) / CTA;
+  lz::lorenz_chain_kernel<OP, INTEG, CTA><<<(unsigned)grid, CTA, 0, st>>>(C, K, Kb, in, out, res, tags, block_ok);
+  return cudaGetLastError();
+}
+
 template <int OP>
 cudaError_t launch_chain(const lz::DevConst& C, const lz::DevKey& K, const lz::DevKey* Kb,
                          uint32_t integrator, const uint8_t* in, uint8_t* out, lorenz_result* res,
                          uint8_t* tags, uint8_t* block_ok, cudaStream_t st) {
-  const uint64_t grid = (C.lanes + lz::kCta - 1) / lz::kCta;
-  if (grid == 0) return cudaSuccess;
+  if (C.lanes == 0) return cudaSuccess;
+  const bool wide = chain_cta(C.lanes, integrator) == 256;
+  if (integrator == LORENZ_RK4_FMA)
+    return launch_chain_cta<OP, LORENZ_RK4_FMA, 128>(C, K, Kb, in, out, res, tags, block_ok, st);
   if (integrator == LORENZ_EULER)
-    lz::lorenz_chain_kernel<OP, LORENZ_EULER><<<(unsigned)grid, lz::kCta, 0, st>>>(C, K, Kb, in, out, res, tags, block_ok);
-  else if (integrator == LORENZ_RK4_FMA)
-    lz::lorenz_chain_kernel<OP, LORENZ_RK4_FMA><<<(unsigned)grid, lz::kCta, 0, st>>>(C, K, Kb, in, out, res, tags,
-                                                                                     block_ok);
-  else
-    lz::lorenz_chain_kernel<OP, LORENZ_RK4><<<(unsigned)grid, lz::kCta, 0, st>>>(C, K, Kb, in, out, res, tags, block_ok);
-  return cudaGetLastError();
+    return wide ? launch_chain_cta<OP, LORENZ_EULER, 256>(C, K, Kb, in, out, res, tags, block_ok, st)
+                : launch_chain_cta<OP, LORENZ_EULER, 128>(C, K, Kb, in, out, res, tags, block_ok, st);
+  return wide ? launch_chain_cta<OP, LORENZ_RK4, 256>(C, K, Kb, in, out, res, tags, block_ok, st)
+              : launch_chain_cta<OP, LORENZ_RK4, 128>(C, K, Kb, in, out, res, tags, block_ok, st);
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }

@@ -418,29 +418,32 @@ __device__ __forceinline__ void st_stream(uint8_t* p, uint4 v) {
 #ifndef LZ_MIN_CTAS
 #define LZ_MIN_CTAS 1
 #endif
-// Resident CTAs per SM (tools/tune.py sweep): RK4 and Euler are at their best with the
-// compiler's register choice (4 CTAs, <= 128 registers); the FMA form gains 2 points
-// (92.7 % -> 94.8 % of the FP64 pipe on C4) from a fifth CTA (<= 102 registers).
-template <int INTEG>
-constexpr int min_ctas() { return INTEG == LORENZ_RK4_FMA ? 5 : LZ_MIN_CTAS; }
+// Resident CTAs per SM (tools/tune.py sweeps). RK4 and Euler: 16 warps per SM (<= 128
+// registers) as 4 CTAs of 128 threads or 2 of 256 — the host picks the CTA size per launch
+// (lorenz.cu: chain_cta). The FMA form gains 2 points (92.7 % -> 94.8 % of the FP64 pipe
+// on C4) from a fifth 128-thread CTA (<= 102 registers).
+template <int INTEG, int CTA>
+constexpr int min_ctas() {
+  return INTEG == LORENZ_RK4_FMA ? 5 : (LZ_MIN_CTAS > 1 ? LZ_MIN_CTAS : 512 / CTA);
+}
 
 // ------------------------------------------------------------------ the kernel
-// OP: OP_ENC / OP_DEC / OP_VERIFY. One lane per block; warps are independent
-// (only __syncwarp), so the CTA never waits on its slowest warp.
-template <int OP, int INTEG>
-__global__ void __launch_bounds__(kCta, min_ctas<INTEG>())
+// OP: OP_ENC / OP_DEC / OP_VERIFY; CTA: 128 or 256 threads. One lane per block; warps are
+// independent (only __syncwarp), so the CTA never waits on its slowest warp.
+template <int OP, int INTEG, int CTA>
+__global__ void __launch_bounds__(CTA, (min_ctas<INTEG, CTA>()))
     lorenz_chain_kernel(const DevConst C, const DevKey K1, const DevKey* __restrict__ Kb,
                         const uint8_t* __restrict__ in, uint8_t* __restrict__ out,
                         lorenz_result* __restrict__ res, uint8_t* __restrict__ tags_batch,
                         uint8_t* __restrict__ block_ok) {
-  __shared__ __align__(16) uint8_t stage[kWarps * 32 * kRow];
+  __shared__ __align__(16) uint8_t stage[(CTA / 32) * 32 * kRow];
   __shared__ double theta_tab[6 * 256];  // RN(p / 10^{3+e}), e = Omega_3 in [0,6), p a byte
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint8_t* wst = stage + warp * 32 * kRow;
-  for (uint32_t i = threadIdx.x; i < 6 * 256; i += kCta)
+  for (uint32_t i = threadIdx.x; i < 6 * 256; i += CTA)
     theta_tab[i] = __ddiv_rn(__uint2double_rn(i & 255), pow10_theta(3 + (i >> 8)));
   __syncthreads();  // the only CTA-wide barrier; warps run independently afterwards
-  const uint64_t g = (uint64_t)blockIdx.x * kCta + threadIdx.x;
+  const uint64_t g = (uint64_t)blockIdx.x * CTA + threadIdx.x;
   const bool active = g < C.lanes;
 
   // lane -> (message s, global block bl)
