@@ -5,6 +5,7 @@
 // caller's stream, and reads back tag / verdict. No CPU fallback: every byte of
 // ciphertext is produced on the GPU.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>  // header-only; ranges are no-ops unless a profiler attaches
 
 #include <cstdio>
 #include <cstring>
@@ -37,6 +38,12 @@ struct KeyImpl {
 static_assert(sizeof(KeyImpl) <= LORENZ_KEY_BYTES, "key layout exceeds the ABI size");
 
 thread_local std::string g_err;
+
+// NVTX range over a host call (tracing for nsys / ncu --nvtx filters)
+struct Trace {
+  explicit Trace(const char* name) { nvtxRangePushA(name); }
+  ~Trace() { nvtxRangePop(); }
+};
 
 const KeyImpl* impl(const lorenz_key* k) {
   if (!k) return nullptr;
@@ -330,6 +337,7 @@ lorenz_status lorenz_result_init_async(lorenz_result* res, void* stream) {
 
 lorenz_status lorenz_encrypt_async(const lorenz_key* k, uint64_t n, uint64_t b0, uint64_t b1,
                                    const uint8_t* pt, uint8_t* ct, lorenz_result* res, void* stream) {
+  Trace tr("lorenz_encrypt");
   const KeyImpl* K = impl(k);
   if (!K || !res) return LORENZ_E_ARG;
   uint64_t ptb = 0, ctb = 0;
@@ -346,6 +354,7 @@ lorenz_status lorenz_encrypt_async(const lorenz_key* k, uint64_t n, uint64_t b0,
 lorenz_status lorenz_decrypt_async(const lorenz_key* k, uint64_t n, uint64_t b0, uint64_t b1,
                                    const uint8_t* ct, uint8_t* pt, uint8_t* block_ok, lorenz_result* res,
                                    void* stream) {
+  Trace tr("lorenz_decrypt");
   const KeyImpl* K = impl(k);
   if (!K || !res) return LORENZ_E_ARG;
   uint64_t ptb = 0, ctb = 0;
@@ -367,6 +376,7 @@ lorenz_status lorenz_decrypt_async(const lorenz_key* k, uint64_t n, uint64_t b0,
 
 lorenz_status lorenz_verify_async(const lorenz_key* k, uint64_t n, uint64_t b0, uint64_t b1, const uint8_t* ct,
                                   lorenz_result* res, void* stream) {
+  Trace tr("lorenz_verify");
   const KeyImpl* K = impl(k);
   if (!K || !res) return LORENZ_E_ARG;
   uint64_t ptb = 0, ctb = 0;
@@ -444,6 +454,7 @@ lorenz_status lorenz_verify(const lorenz_key* k, uint64_t n, uint64_t b0, uint64
 
 lorenz_status lorenz_encrypt_batch(const lorenz_key* keys, uint32_t S, uint64_t n, const uint8_t* pts,
                                    uint8_t* cts, uint8_t* tags, void* stream) {
+  Trace tr("lorenz_encrypt_batch");
   if (!keys || S == 0) return LORENZ_E_ARG;
   const KeyImpl* K0 = impl(&keys[0]);
   if (!K0) return LORENZ_E_ARG;
@@ -497,6 +508,7 @@ lorenz_status lorenz_encrypt_batch(const lorenz_key* keys, uint32_t S, uint64_t 
 lorenz_status lorenz_digit_histograms(const double* ic, uint64_t lanes, uint32_t skip, uint32_t samples,
                                       uint32_t stride, uint32_t dt_code, uint32_t integrator, uint64_t* hist,
                                       void* stream) {
+  Trace tr("lorenz_digit_histograms");
   if (!hist || (lanes && !ic) || dt_code > 3 || integrator > 2 || lanes > (1ULL << 40)) return LORENZ_E_ARG;
   cudaStream_t st = (cudaStream_t)stream;
   if (!cuda_ok(cudaMemsetAsync(hist, 0, sizeof(uint64_t) * lz::kHistBins, st), "memset")) return LORENZ_E_CUDA;
@@ -620,6 +632,7 @@ uint32_t auto_chunks(uint64_t nb, uint32_t req) {
 // Blocks [B0,B1) from host slices: chunked H2D -> kernel -> D2H over HostPipe's streams.
 static lorenz_status host_range(const lorenz_key* k, uint64_t n, uint64_t B0, uint64_t B1, const uint8_t* in_host,
                                 uint8_t* out_host, bool decrypt, lorenz_result* h_res, uint32_t n_chunks) {
+  Trace tr(decrypt ? "lorenz_decrypt_host" : "lorenz_encrypt_host");
   const KeyImpl* K = impl(k);
   if (!K) return LORENZ_E_ARG;
   uint64_t ptb = 0, ctb = 0;
