@@ -236,6 +236,19 @@ def test_thread_invariance_and_ranges(ref):
     assert x.tobytes() == t1
 
 
+def test_encrypt_block_equals_message_slice(ref):
+    """encrypt_block (used for sampled GPU parity at full size) reproduces the block's slice
+    of the whole-message ciphertext, including the ragged last block."""
+    rng = random.Random(15)
+    pt = rng.randbytes(5 * 1024 + 300)
+    prm = _P(ref.FAST, 12)
+    whole, _ = ref.encrypt(b"block-pw", pt, prm)
+    for b in range(6):
+        blk = np.frombuffer(pt[b * 1024:(b + 1) * 1024], np.uint8)
+        got = ref.encrypt_block(b"block-pw", len(pt), b, blk, prm)
+        assert np.array_equal(got, whole[b * 1040: b * 1040 + len(blk) + 16])
+
+
 def test_fast_single_block_equals_strong_under_subkey(ref):
     """a single-block FAST message equals STRONG encryption under the block-0
     sub-password with the FAST n_it."""
