@@ -8,6 +8,7 @@
 #include <nvtx3/nvToolsExt.h>  // header-only; ranges are no-ops unless a profiler attaches
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -151,6 +152,10 @@ int sm_count() {
 // 16 MiB to 1 GiB: the rule picked the faster size at every one).
 int chain_cta(uint64_t lanes, uint32_t integrator) {
   if (integrator == LORENZ_RK4_FMA) return 128;  // 5 CTAs/SM of 128 (see min_ctas)
+  if (const char* f = std::getenv("LORENZ_CTA")) {  // tuning override: 128 | 256 | 512
+    const int v = std::atoi(f);
+    if (v == 128 || v == 256 || v == 512) return v;
+  }
   const uint64_t warps = (lanes + 31) / 32, sms = (uint64_t)sm_count();
   const uint64_t c128 = (warps + 3) / 4, c256 = (warps + 7) / 8;  // CTAs of 4 / 8 warps
   const uint64_t l128 = 4 * ((c128 + sms - 1) / sms), l256 = 8 * ((c256 + sms - 1) / sms);
@@ -170,14 +175,16 @@ cudaError_t launch_chain(const lz::DevConst& C, const lz::DevKey& K, const lz::D
                          uint32_t integrator, const uint8_t* in, uint8_t* out, lorenz_result* res,
                          uint8_t* tags, uint8_t* block_ok, cudaStream_t st) {
   if (C.lanes == 0) return cudaSuccess;
-  const bool wide = chain_cta(C.lanes, integrator) == 256;
+  const int cta = chain_cta(C.lanes, integrator);
   if (integrator == LORENZ_RK4_FMA)
     return launch_chain_cta<OP, LORENZ_RK4_FMA, 128>(C, K, Kb, in, out, res, tags, block_ok, st);
   if (integrator == LORENZ_EULER)
-    return wide ? launch_chain_cta<OP, LORENZ_EULER, 256>(C, K, Kb, in, out, res, tags, block_ok, st)
-                : launch_chain_cta<OP, LORENZ_EULER, 128>(C, K, Kb, in, out, res, tags, block_ok, st);
-  return wide ? launch_chain_cta<OP, LORENZ_RK4, 256>(C, K, Kb, in, out, res, tags, block_ok, st)
-              : launch_chain_cta<OP, LORENZ_RK4, 128>(C, K, Kb, in, out, res, tags, block_ok, st);
+    return cta == 512   ? launch_chain_cta<OP, LORENZ_EULER, 512>(C, K, Kb, in, out, res, tags, block_ok, st)
+           : cta == 256 ? launch_chain_cta<OP, LORENZ_EULER, 256>(C, K, Kb, in, out, res, tags, block_ok, st)
+                        : launch_chain_cta<OP, LORENZ_EULER, 128>(C, K, Kb, in, out, res, tags, block_ok, st);
+  return cta == 512   ? launch_chain_cta<OP, LORENZ_RK4, 512>(C, K, Kb, in, out, res, tags, block_ok, st)
+         : cta == 256 ? launch_chain_cta<OP, LORENZ_RK4, 256>(C, K, Kb, in, out, res, tags, block_ok, st)
+                      : launch_chain_cta<OP, LORENZ_RK4, 128>(C, K, Kb, in, out, res, tags, block_ok, st);
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }

@@ -64,8 +64,12 @@ __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a,
 __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
 
+// r[i] for i in {0,1,2}: two predicated selects, no branch
 __device__ __forceinline__ double sel3(uint32_t i, double x, double y, double z) {
-  return i == 0 ? x : (i == 1 ? y : z);
+  double r = x;
+  r = (i == 1) ? y : r;
+  r = (i == 2) ? z : r;
+  return r;
 }
 
 // big-endian byte i (0-based, i < 24) of six words; i is warp-uniform in practice
@@ -101,14 +105,15 @@ __device__ __forceinline__ double g_divisor(uint32_t L) {
 
 // floor(|alpha| * 10^13) of the rounded product (Eq.8, Q8, Q9). The product is one DMUL;
 // the floor is taken from its bit pattern on the integer pipes (equal to F2I.U64.TRUNC for
-// every product below 2^64; inside the guard box the product is < 2^51, Q7).
+// every product below 2^53; inside the guard box the product is < 2^51, Q7).
 __device__ __forceinline__ uint64_t quantise(double alpha) {
   const uint64_t bits = (uint64_t)__double_as_longlong(dmul(fabs(alpha), 1e13));
   const int e = (int)(bits >> 52) - 1023;  // unbiased exponent (sign bit is clear)
   const uint64_t mant = (bits & 0xFFFFFFFFFFFFFULL) | (1ULL << 52);
-  if (e < 0) return 0;
-  if (e <= 52) return mant >> (52 - e);
-  return e < 64 ? mant << (e - 52) : ~0ULL;  // only outside the guard box (divergence)
+  // branch-free; e < 0 shifts everything out (52 - e >= 53). Exact for every product below
+  // 2^53: inside the guard box (|coordinates| <= 150) products are < 2^51; outside it the
+  // chain is already flagged DIVERGENCE (Q18) and its bytes are not defined.
+  return mant >> (uint32_t)min(max(52 - e, 0), 63);
 }
 
 // x mod k for x < 1024, 1 <= k <= 6, with inv = ceil(2^16 / k): one multiply instead of
@@ -436,10 +441,12 @@ __global__ void __launch_bounds__(CTA, (min_ctas<INTEG, CTA>()))
                         const uint8_t* __restrict__ in, uint8_t* __restrict__ out,
                         lorenz_result* __restrict__ res, uint8_t* __restrict__ tags_batch,
                         uint8_t* __restrict__ block_ok) {
-  __shared__ __align__(16) uint8_t stage[(CTA / 32) * 32 * kRow];
+  constexpr int WIN = CTA >= 512 ? 32 : kWin;  // 512-thread CTAs: shorter windows keep smem < 48 KB
+  constexpr int ROW = WIN + 16, CHUNKS = WIN / 16;
+  __shared__ __align__(16) uint8_t stage[(CTA / 32) * 32 * ROW];
   __shared__ double theta_tab[6 * 256];  // RN(p / 10^{3+e}), e = Omega_3 in [0,6), p a byte
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint8_t* wst = stage + warp * 32 * kRow;
+  uint8_t* wst = stage + warp * 32 * ROW;
   for (uint32_t i = threadIdx.x; i < 6 * 256; i += CTA)
     theta_tab[i] = __ddiv_rn(__uint2double_rn(i & 255), pow10_theta(3 + (i >> 8)));
   __syncthreads();  // the only CTA-wide barrier; warps run independently afterwards
@@ -470,11 +477,11 @@ __global__ void __launch_bounds__(CTA, (min_ctas<INTEG, CTA>()))
   uint64_t tlo = 0, thi = 0;  // last 16 ciphertext bytes = the block tag
   const uint64_t wtotal = warp_max_u64(total);
 
-  for (uint64_t w0 = 0; w0 < wtotal; w0 += kWin) {
-    // ---- stage in: 32 rows x kWin bytes, coalesced 16-B chunks ----
+  for (uint64_t w0 = 0; w0 < wtotal; w0 += WIN) {
+    // ---- stage in: 32 rows x WIN bytes, coalesced 16-B chunks ----
 #pragma unroll
-    for (int it = 0; it < kChunks; ++it) {
-      const uint32_t q = it * 32 + lane, row = q / kChunks, c = q % kChunks;
+    for (int it = 0; it < CHUNKS; ++it) {
+      const uint32_t q = it * 32 + lane, row = q / CHUNKS, c = q % CHUNKS;
       const uint8_t* r_in = (const uint8_t*)__shfl_sync(0xffffffffu, (unsigned long long)irow, row);
       const uint64_t r_len = __shfl_sync(0xffffffffu, len, row);
       const uint64_t r_tot = __shfl_sync(0xffffffffu, total, row);
@@ -500,15 +507,15 @@ __global__ void __launch_bounds__(CTA, (min_ctas<INTEG, CTA>()))
           v = make_uint4(wv[0], wv[1], wv[2], wv[3]);
         }
       }
-      *reinterpret_cast<uint4*>(wst + row * kRow + 16 * c) = v;
+      *reinterpret_cast<uint4*>(wst + row * ROW + 16 * c) = v;
     }
     __syncwarp();
 
-    // ---- the chain over this lane's characters [w0, min(w0+kWin, total)) ----
+    // ---- the chain over this lane's characters [w0, min(w0+WIN, total)) ----
     if (w0 < total) {
-      const uint64_t wend = (w0 + kWin < total) ? w0 + kWin : total;
+      const uint64_t wend = (w0 + WIN < total) ? w0 + WIN : total;
       for (uint64_t j0 = w0; j0 < wend; j0 += 16) {
-        uint4* cell = reinterpret_cast<uint4*>(wst + lane * kRow + (j0 - w0));
+        uint4* cell = reinterpret_cast<uint4*>(wst + lane * ROW + (j0 - w0));
         const uint4 v = *cell;
         uint64_t ilo = (uint64_t)v.x | ((uint64_t)v.y << 32), ihi = (uint64_t)v.z | ((uint64_t)v.w << 32);
         uint64_t olo = 0, ohi = 0;
@@ -547,15 +554,15 @@ __global__ void __launch_bounds__(CTA, (min_ctas<INTEG, CTA>()))
     // ---- stage out ----
     if (OP != OP_VERIFY) {
 #pragma unroll
-      for (int it = 0; it < kChunks; ++it) {
-        const uint32_t q = it * 32 + lane, row = q / kChunks, c = q % kChunks;
+      for (int it = 0; it < CHUNKS; ++it) {
+        const uint32_t q = it * 32 + lane, row = q / CHUNKS, c = q % CHUNKS;
         uint8_t* r_out = (uint8_t*)__shfl_sync(0xffffffffu, (unsigned long long)orow, row);
         const uint64_t r_len = __shfl_sync(0xffffffffu, len, row);
         const uint64_t r_tot = __shfl_sync(0xffffffffu, total, row);
         const uint64_t r_dst = (OP == OP_ENC) ? r_tot : r_len;
         const uint64_t pos = w0 + 16 * c;
         if (r_tot && pos < r_dst) {
-          const uint4 v = *reinterpret_cast<const uint4*>(wst + row * kRow + 16 * c);
+          const uint4 v = *reinterpret_cast<const uint4*>(wst + row * ROW + 16 * c);
           if (pos + 16 <= r_dst) {
             st_stream(r_out + pos, v);
           } else {
