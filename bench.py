@@ -244,18 +244,22 @@ def run_c5(a):
     if dist_on:
         dist.barrier()
     evs = []
-    for _ in range(a.steps):
-        flush.fill_(1)
-        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-        e[0].record()
-        bt.encrypt()
-        e[1].record()
-        bt.statistics()
-        e[2].record()
-        evs.append(e)
-    torch.cuda.synchronize()
+    gpu_uuid = str(torch.cuda.get_device_properties(dev).uuid)
+    with ClockSampler(gpu_uuid if gpu_uuid.startswith("GPU-") else "GPU-" + gpu_uuid) as clk:
+        for _ in range(a.steps):
+            flush.fill_(1)
+            e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            e[0].record()
+            bt.encrypt()
+            e[1].record()
+            bt.statistics()
+            e[2].record()
+            evs.append(e)
+        torch.cuda.synchronize()
+    clocks = clk.summary()
     step_ms = [e[0].elapsed_time(e[2]) for e in evs]
     enc_ms = [e[0].elapsed_time(e[1]) for e in evs]
+    stats_ms = [e[1].elapsed_time(e[2]) for e in evs]
 
     def mx(x):
         if not dist_on:
@@ -281,11 +285,13 @@ def run_c5(a):
             "roofline": {"bound": "alu", "achieved": round(achieved, 4), "peak": round(peak, 4),
                          "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": None,
                          "kernel": "lz::lorenz_chain_kernel<ENC,RK4> (batch)"},
+            "phase_ms": {"encrypt": [round(x, 2) for x in enc_ms], "statistics": [round(x, 2) for x in stats_ms]},
             "c5_stats_rank0": {"pw_flip_bit_diff_mean": float(pw_bits.mean()),
                                "ct_entropy_min": float(min(ent)),
                                "untouched_blocks_identical": bool((co[:, 2, 1] + co[:, 3, 1]).max() == 0),
                                "locked_block_fraction": float((lo[:, :, 2] == B - sweep.LOCK_FROM).mean())},
             "gpu_launches": a.steps * (1 + 2 + 1 + -(-len(bt.lsb_spans) // 65535)),
+            "clocks": clocks,
             "e2e": None,
         }), flush=True)
     if dist_on:
