@@ -218,7 +218,23 @@ lorenz_status finish_sync(lorenz_result* d_res, cudaStream_t st, lorenz_result* 
   return LORENZ_OK;
 }
 
+// The library's small per-call buffers come from the device's stream-ordered pool. With the
+// default release threshold (0) every synchronisation hands freed pages back to the driver
+// and the next call maps them again; keep them cached instead (once per device).
+void keep_pool_cached() {
+  static bool done[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64 || done[dev]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = ~0ULL;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done[dev] = true;
+}
+
 lorenz_status alloc_result(lorenz_result** d_res, cudaStream_t st) {
+  keep_pool_cached();
   if (!cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(d_res), sizeof(lorenz_result), st), "cudaMallocAsync"))
     return LORENZ_E_CUDA;
   lz::result_init_kernel<<<1, 32, 0, st>>>(*d_res);
@@ -544,6 +560,7 @@ namespace {
 template <typename Launch>
 lorenz_status span_launch(const lorenz_span* spans, uint32_t count, uint64_t* out, uint64_t out_words,
                           cudaStream_t st, Launch launch) {
+  keep_pool_cached();
   if (!cuda_ok(cudaMemsetAsync(out, 0, sizeof(uint64_t) * out_words, st), "memset")) return LORENZ_E_CUDA;
   uint64_t mx = 0;
   for (uint32_t i = 0; i < count; ++i) mx = spans[i].len > mx ? spans[i].len : mx;
@@ -592,17 +609,7 @@ struct HostPipe {
   cudaStream_t st[kStreams] = {};
   cudaEvent_t ev[kStreams] = {};
   bool init() {
-    static bool pool_set = false;
-    if (!pool_set) {  // keep freed stream-ordered memory cached across calls
-      int dev = 0;
-      cudaGetDevice(&dev);
-      cudaMemPool_t pool;
-      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        uint64_t thr = ~0ULL;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-      }
-      pool_set = true;
-    }
+    keep_pool_cached();  // freed stream-ordered memory stays cached across calls
     for (int i = 0; i < kStreams; ++i) {
       if (!cuda_ok(cudaStreamCreateWithFlags(&st[i], cudaStreamNonBlocking), "stream create")) return false;
       if (!cuda_ok(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming), "event create")) return false;
