@@ -221,6 +221,39 @@ def test_async_api_and_result_slot():
     assert int(r[16:24].view(np.uint64)[0]) == 2 ** 64 - 1 and int(r[24:28].view(np.uint32)[0]) == 0
 
 
+def test_async_calls_capture_into_a_cuda_graph():
+    """The _async calls enqueue only kernels (no allocation, no sync): a whole
+    init -> encrypt -> init -> decrypt sequence is captured once and replayed."""
+    pw = inputs.password()
+    n = 6 * 1024 + 3
+    msg = inputs.message(n)
+    key = L.lorenz_keysetup(pw, mode=L.FAST, n_it=5)
+    nb = key.num_blocks(n)
+    pt = torch.from_numpy(msg).to(DEV)
+    ct = torch.empty(key.ct_len(n), dtype=torch.uint8, device=DEV)
+    back = torch.empty(n, dtype=torch.uint8, device=DEV)
+    res = torch.empty(64, dtype=torch.uint8, device=DEV)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        L.lorenz_result_init_async(res[:32], stream=s)
+        L.lorenz_encrypt_async(key, n, 0, nb, pt, ct, res[:32], stream=s)
+        L.lorenz_result_init_async(res[32:], stream=s)
+        L.lorenz_decrypt_async(key, n, 0, nb, ct, back, res[32:], stream=s)
+    want, want_tag = oracle.encrypt(pw, msg, oparams(key))
+    for _ in range(2):
+        ct.zero_()
+        back.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        assert np.array_equal(ct.cpu().numpy(), want)
+        r = res.cpu().numpy()
+        assert r[:16].tobytes() == want_tag
+        assert int(r[48:56].view(np.uint64)[0]) == 2 ** 64 - 1  # no failing block
+        assert torch.equal(back, pt)
+
+
 def test_host_buffer_end_to_end():
     pw = inputs.password()
     n = 50 * 1024 + 9
