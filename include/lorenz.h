@@ -195,10 +195,12 @@ lorenz_status lorenz_digit_histograms(const double* ic, uint64_t lanes, uint32_t
  * blocks [b0,b1) of an n-byte message; pt_host / ct_host are HOST pointers to the
  * slice starts (same slice convention as the device calls; [0, num_blocks) is the
  * whole message). Host->device copies, kernels and device->host copies are
- * pipelined over `n_chunks` block-aligned chunks on internal streams (0 ->
- * automatic) on the current device. Pinned host memory gives overlapped copies;
- * pageable memory works but copies synchronously. Allocates its own device buffers
- * from the stream-ordered pool (kept cached between calls). Synchronous.
+ * pipelined over `n_chunks` block-aligned chunks (0 -> automatic: max(8, slice/128 MiB))
+ * on the current device. Chunk c runs on internal stream c % S, S = min(8, chunks), whose
+ * device buffers hold one chunk and are reused in stream order, so device memory is
+ * bounded by ~2 x S chunks whatever the slice size (slices larger than HBM work).
+ * Pinned host memory gives overlapped copies; pageable memory works but copies
+ * synchronously. Buffers come from the stream-ordered pool (kept cached). Synchronous.
  * decrypt: on LORENZ_E_INTEGRITY the whole host plaintext slice is zero-filled. */
 lorenz_status lorenz_encrypt_host(const lorenz_key* k, uint64_t n, uint64_t b0, uint64_t b1,
                                   const uint8_t* pt_host, uint8_t* ct_host, uint8_t tag_xor[16],

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 #include <nvtx3/nvToolsExt.h>  // header-only; ranges are no-ops unless a profiler attaches
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -636,14 +637,15 @@ struct HostPipe {
   }
 };
 
-uint32_t auto_chunks(uint64_t nb, uint32_t req) {
-  uint64_t c = req ? req : 8;
-  if (c > nb) c = nb;
-  return (uint32_t)(c ? c : 1);
-}
+constexpr uint64_t kHostChunk = 128ull << 20;  // upper bound of an automatic host-path chunk
 }  // namespace
 
 // Blocks [B0,B1) from host slices: chunked H2D -> kernel -> D2H over HostPipe's streams.
+// Blocks [B0,B1) from host slices. The slice is cut into block-aligned chunks (default: at least
+// 8, at most ~128 MiB each); chunk c runs on slot c % S (S = min(8, chunks)), each slot owning a
+// stream and device buffers sized for one chunk. Chunk c + S reuses the slot's buffers only
+// after chunk c's D2H (same stream), so the host never waits and device memory stays bounded
+// (≈ 8 x 2 x 128 MiB) whatever the message size: messages larger than HBM work.
 static lorenz_status host_range(const lorenz_key* k, uint64_t n, uint64_t B0, uint64_t B1, const uint8_t* in_host,
                                 uint8_t* out_host, bool decrypt, lorenz_result* h_res, uint32_t n_chunks) {
   Trace tr(decrypt ? "lorenz_decrypt_host" : "lorenz_encrypt_host");
@@ -654,43 +656,60 @@ static lorenz_status host_range(const lorenz_key* k, uint64_t n, uint64_t B0, ui
   const uint64_t inb = decrypt ? ctb : ptb, outb = decrypt ? ptb : ctb;
   lorenz_status ret = check_range(K, n, B0, B1, in_host, inb, out_host, outb);
   if (ret != LORENZ_OK || B0 == B1) return ret;
+  const uint64_t nbk = B1 - B0;
+  uint64_t C = n_chunks ? n_chunks : std::max<uint64_t>(8, (inb + kHostChunk - 1) / kHostChunk);
+  if (C > nbk) C = nbk;
+  const uint32_t S = (uint32_t)std::min<uint64_t>(C, HostPipe::kStreams);
+  const uint64_t Bsz = block_B(K, n);
+  uint64_t cap_in = 16, cap_out = 16, cap_blk = 1;  // the largest chunk
+  for (uint64_t c = 0; c < C; ++c) {
+    const uint64_t b0 = B0 + nbk * c / C, b1 = B0 + nbk * (c + 1) / C;
+    uint64_t cp, cc;
+    slice_bytes(K, n, b0, b1, &cp, &cc);
+    cap_in = std::max(cap_in, decrypt ? cc : cp);
+    cap_out = std::max(cap_out, decrypt ? cp : cc);
+    cap_blk = std::max(cap_blk, b1 - b0);
+  }
   HostPipe P;
   if (!P.init()) return LORENZ_E_CUDA;
-  uint8_t *d_in = nullptr, *d_out = nullptr, *d_ok = nullptr;
+  uint8_t *d_in[HostPipe::kStreams] = {}, *d_out[HostPipe::kStreams] = {}, *d_ok[HostPipe::kStreams] = {};
   lorenz_result* d_res = nullptr;
   cudaStream_t s0 = P.st[0];
-  if (!cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&d_in), inb ? inb : 16, s0), "alloc in") ||
-      !cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&d_out), outb ? outb : 16, s0), "alloc out") ||
-      (decrypt && !cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&d_ok), B1 - B0, s0), "alloc ok")))
-    ret = LORENZ_E_CUDA;
+  for (uint32_t i = 0; i < S && ret == LORENZ_OK; ++i)
+    if (!cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&d_in[i]), cap_in, s0), "alloc in") ||
+        !cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&d_out[i]), cap_out, s0), "alloc out") ||
+        (decrypt && !cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&d_ok[i]), cap_blk, s0), "alloc ok")))
+      ret = LORENZ_E_CUDA;
   if (ret == LORENZ_OK) ret = alloc_result(&d_res, s0);
   if (ret == LORENZ_OK) {
     P.fan_out();
-    const uint32_t C = auto_chunks(B1 - B0, n_chunks);
-    const uint64_t Bsz = block_B(K, n);
-    for (uint32_t c = 0; c < C && ret == LORENZ_OK; ++c) {
-      const uint64_t b0 = B0 + (B1 - B0) * c / C, b1 = B0 + (B1 - B0) * (c + 1) / C;
+    for (uint64_t c = 0; c < C && ret == LORENZ_OK; ++c) {
+      const uint64_t b0 = B0 + nbk * c / C, b1 = B0 + nbk * (c + 1) / C;
       if (b0 == b1) continue;
-      cudaStream_t st = P.st[c % HostPipe::kStreams];
+      const uint32_t sl = (uint32_t)(c % S);
+      cudaStream_t st = P.st[sl];
       uint64_t cp, cc;
       slice_bytes(K, n, b0, b1, &cp, &cc);
       const uint64_t poff = (b0 - B0) * Bsz, coff = poff + 16 * (b0 - B0);  // offsets inside the slice
       const uint64_t ioff = decrypt ? coff : poff, ooff = decrypt ? poff : coff;
       const uint64_t ib = decrypt ? cc : cp, ob = decrypt ? cp : cc;
-      if (ib && !cuda_ok(cudaMemcpyAsync(d_in + ioff, in_host + ioff, ib, cudaMemcpyHostToDevice, st), "H2D")) {
-        ret = LORENZ_E_CUDA; break;
+      if (ib && !cuda_ok(cudaMemcpyAsync(d_in[sl], in_host + ioff, ib, cudaMemcpyHostToDevice, st), "H2D")) {
+        ret = LORENZ_E_CUDA;
+        break;
       }
-      ret = decrypt ? lorenz_decrypt_async(k, n, b0, b1, d_in + ioff, d_out + ooff, d_ok + (b0 - B0), d_res, st)
-                    : lorenz_encrypt_async(k, n, b0, b1, d_in + ioff, d_out + ooff, d_res, st);
+      ret = decrypt ? lorenz_decrypt_async(k, n, b0, b1, d_in[sl], d_out[sl], d_ok[sl], d_res, st)
+                    : lorenz_encrypt_async(k, n, b0, b1, d_in[sl], d_out[sl], d_res, st);
       if (ret == LORENZ_OK && ob &&
-          !cuda_ok(cudaMemcpyAsync(out_host + ooff, d_out + ooff, ob, cudaMemcpyDeviceToHost, st), "D2H"))
+          !cuda_ok(cudaMemcpyAsync(out_host + ooff, d_out[sl], ob, cudaMemcpyDeviceToHost, st), "D2H"))
         ret = LORENZ_E_CUDA;
     }
     P.fan_in();
   }
-  if (d_in) cudaFreeAsync(d_in, s0);
-  if (d_out) cudaFreeAsync(d_out, s0);
-  if (d_ok) cudaFreeAsync(d_ok, s0);
+  for (uint32_t i = 0; i < S; ++i) {
+    if (d_in[i]) cudaFreeAsync(d_in[i], s0);
+    if (d_out[i]) cudaFreeAsync(d_out[i], s0);
+    if (d_ok[i]) cudaFreeAsync(d_ok[i], s0);
+  }
   if (d_res) {
     lorenz_status f = finish_sync(d_res, s0, h_res);
     if (ret == LORENZ_OK) ret = f;

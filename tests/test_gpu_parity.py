@@ -278,6 +278,29 @@ def test_host_buffer_end_to_end():
     assert st == L.E_INTEGRITY and fb == 20 and not back.any()
 
 
+@pytest.mark.parametrize("chunks", [9, 17, 51])
+def test_host_buffer_ring_reuse(chunks):
+    """More chunks than the 8 device slots: chunk c reuses slot c % 8's buffers after chunk c-8's
+    D2H (stream order). Ragged chunks (51 blocks into 17 / 9), last block partial."""
+    pw = inputs.password()
+    n = 50 * 1024 + 777
+    msg = inputs.message(n, seed=11)
+    key = L.lorenz_keysetup(pw, mode=L.FAST, n_it=5)
+    nb = key.num_blocks(n)
+    ct_h = np.zeros(key.ct_len(n), dtype=np.uint8)
+    tag = L.lorenz_encrypt_host(key, n, 0, nb, msg, ct_h, n_chunks=chunks)
+    want, want_tag = oracle.encrypt(pw, msg, oparams(key))
+    assert np.array_equal(ct_h, want) and tag == want_tag
+    back = np.zeros(n, dtype=np.uint8)
+    st, fb = L.lorenz_decrypt_host(key, n, 0, nb, ct_h, back, n_chunks=chunks)
+    assert st == L.OK and fb == -1 and np.array_equal(back, msg)
+    bad = ct_h.copy()
+    bad[47 * 1040 + 1039] ^= 1  # a tag byte of block 47: a late lap of the ring
+    bad[44 * 1040 + 5] ^= 0x80
+    st, fb = L.lorenz_decrypt_host(key, n, 0, nb, bad, back, n_chunks=chunks)
+    assert st == L.E_INTEGRITY and fb == 44 and not back.any()
+
+
 def test_argument_errors():
     key = L.lorenz_keysetup(b"password", mode=L.FAST)
     n = 4096
