@@ -105,6 +105,15 @@ def lib():
                                          C.c_uint64, C.c_void_p, C.c_void_p, u8p, C.c_int]
         L.lorenz_ref_digit_hist.argtypes = [C.c_void_p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32,
                                             C.c_uint32, C.c_uint32, C.c_void_p]
+        u32 = C.c_uint32
+        L.lorenz_ref_autocorr.argtypes = [C.c_void_p, u32, u32, C.c_void_p]
+        L.lorenz_ref_autocorr_at.argtypes = [C.c_void_p, u32, u32, u32, u32]
+        L.lorenz_ref_autocorr_at.restype = C.c_double
+        L.lorenz_ref_power_spectrum.argtypes = [C.c_void_p, u32, u32, C.c_void_p]
+        L.lorenz_ref_power_at.argtypes = [C.c_void_p, u32, u32, u32, u32]
+        L.lorenz_ref_power_at.restype = C.c_double
+        L.lorenz_ref_spectral_flatness.argtypes = [C.c_void_p, u32, u32]
+        L.lorenz_ref_spectral_flatness.restype = C.c_double
         L.lorenz_ref_encrypt_block.argtypes = [C.c_char_p, C.c_size_t, C.POINTER(Params), C.c_uint64,
                                                C.c_uint64, C.c_void_p, C.c_void_p]
         L.lorenz_ref_decrypt.argtypes = [C.c_char_p, C.c_size_t, C.POINTER(Params), C.c_uint64, C.c_uint64,
@@ -316,6 +325,45 @@ def digit_hist(ic: np.ndarray, skip: int, samples: int, stride: int, dt_code=0, 
     lib().lorenz_ref_digit_hist(ic.ctypes.data, ic.shape[0], skip, samples, stride, dt_code, integrator,
                                 hist.ctypes.data)
     return hist
+
+
+def _image(x) -> np.ndarray:
+    a = np.ascontiguousarray(x, dtype=np.uint8)
+    if a.ndim != 2:
+        raise ValueError("expected an H x W uint8 matrix")
+    return a
+
+
+def autocorr(x) -> np.ndarray:
+    """Fig.3: normalised circular 2-D autocorrelation r[u, v] of an H x W byte matrix (Q25)."""
+    a = _image(x)
+    r = np.zeros(a.shape, dtype=np.float64)
+    lib().lorenz_ref_autocorr(a.ctypes.data, a.shape[0], a.shape[1], r.ctypes.data)
+    return r
+
+
+def autocorr_at(x, u: int, v: int) -> float:
+    a = _image(x)
+    return lib().lorenz_ref_autocorr_at(a.ctypes.data, a.shape[0], a.shape[1], u, v)
+
+
+def power_spectrum(x) -> np.ndarray:
+    """Fig.4 (g)-(i): |2-D DFT|^2 / N^2, DC-centred (Q26)."""
+    a = _image(x)
+    p = np.zeros(a.shape, dtype=np.float64)
+    lib().lorenz_ref_power_spectrum(a.ctypes.data, a.shape[0], a.shape[1], p.ctypes.data)
+    return p
+
+
+def power_at(x, k: int, l: int) -> float:
+    """One frequency (k, l), unshifted indices, of power_spectrum."""
+    a = _image(x)
+    return lib().lorenz_ref_power_at(a.ctypes.data, a.shape[0], a.shape[1], k, l)
+
+
+def spectral_flatness(p) -> float:
+    p = np.ascontiguousarray(p, dtype=np.float64)
+    return lib().lorenz_ref_spectral_flatness(p.ctypes.data, p.shape[0], p.shape[1])
 
 
 def encrypt_block(pw: bytes, n: int, b: int, blk_pt, prm: Params) -> np.ndarray:

@@ -722,3 +722,117 @@ int lorenz_ref_decrypt(const uint8_t* pw, size_t pw_len, const lref_params* prm_
   free(ok);
   return *first_bad >= 0 ? LREF_E_INTEGRITY : LREF_OK;
 }
+
+/* ======================================================================== */
+/* NEXT-4 analysis suite: the §4 statistics of the paper's Figs. 3 and 4.    */
+/* Plain definitions, O(N) per output, O(N^2) per matrix (N = H*W).          */
+/* ======================================================================== */
+
+/* mean-centred samples d = x - mean(x) ("auto-correlation matrices"; S:434 mean-center) */
+static double* centred(const uint8_t* x, uint64_t N) {
+  double* d = (double*)malloc((size_t)N * sizeof(double));
+  double sum = 0.0;
+  for (uint64_t i = 0; i < N; ++i) sum += (double)x[i];
+  const double mean = sum / (double)N;
+  for (uint64_t i = 0; i < N; ++i) d[i] = (double)x[i] - mean;
+  return d;
+}
+
+static double autocorr_lag(const double* d, uint32_t H, uint32_t W, uint32_t u, uint32_t v, double var) {
+  if (var == 0.0) return (u == 0 && v == 0) ? 1.0 : 0.0; /* constant input: S:436 convention (Q25) */
+  double c = 0.0;
+  for (uint32_t i = 0; i < H; ++i)
+    for (uint32_t j = 0; j < W; ++j)
+      c += d[(uint64_t)i * W + j] * d[(uint64_t)((i + u) % H) * W + (j + v) % W];
+  return c / var;
+}
+
+static double centred_var(const double* d, uint64_t N) {
+  double var = 0.0;
+  for (uint64_t i = 0; i < N; ++i) var += d[i] * d[i];
+  return var;
+}
+
+/* Normalised circular 2-D autocorrelation of the H x W byte matrix x (row-major), Fig.3 / Q25:
+ * r(u,v) = sum_{i,j} d[i][j] d[(i+u) mod H][(j+v) mod W] / sum_{i,j} d[i][j]^2,  d = x - mean(x).
+ * r[u*W + v]; lag (0,0) at index 0.                                                         */
+void lorenz_ref_autocorr(const uint8_t* x, uint32_t H, uint32_t W, double* r) {
+  const uint64_t N = (uint64_t)H * W;
+  double* d = centred(x, N);
+  const double var = centred_var(d, N);
+  for (uint32_t u = 0; u < H; ++u)
+    for (uint32_t v = 0; v < W; ++v) r[(uint64_t)u * W + v] = autocorr_lag(d, H, W, u, v, var);
+  free(d);
+}
+
+/* one lag of the same matrix (for sampled checks at sizes where the full matrix is too slow) */
+double lorenz_ref_autocorr_at(const uint8_t* x, uint32_t H, uint32_t W, uint32_t u, uint32_t v) {
+  const uint64_t N = (uint64_t)H * W;
+  double* d = centred(x, N);
+  const double r = autocorr_lag(d, H, W, u, v, centred_var(d, N));
+  free(d);
+  return r;
+}
+
+#define LREF_TWO_PI 6.283185307179586476925286766559
+/* Power of the 2-D DFT at frequency (k,l), Fig.4 (g)-(i) / Q26:
+ * F(k,l) = sum_{m,n} x[m][n] exp(-2 pi i (k m / H + l n / W)) = sum x exp(-2 pi i t / N),
+ * t = (k m W + l n H) mod N;  P = |F|^2 / N^2 (so sum P = mean(x^2), Parseval).
+ * cs: optional table cos/sin(2 pi t / N) for t < N (interleaved), else computed per term.   */
+static double power_bin(const uint8_t* x, uint32_t H, uint32_t W, uint32_t k, uint32_t l, const double* cs) {
+  const uint64_t N = (uint64_t)H * W;
+  double re = 0.0, im = 0.0;
+  for (uint32_t m = 0; m < H; ++m)
+    for (uint32_t n = 0; n < W; ++n) {
+      const uint64_t t = ((uint64_t)k * m % H * W + (uint64_t)l * n % W * H) % N;
+      double c, s;
+      if (cs) {
+        c = cs[2 * t];
+        s = cs[2 * t + 1];
+      } else {
+        const double a = LREF_TWO_PI * (double)t / (double)N;
+        c = cos(a);
+        s = sin(a);
+      }
+      const double v = (double)x[(uint64_t)m * W + n];
+      re += v * c;
+      im -= v * s;
+    }
+  const double N2 = (double)N * (double)N;
+  return (re * re + im * im) / N2;
+}
+
+/* Full power spectrum, DC-centred: P(k,l) stored at ((k + H/2) mod H, (l + W/2) mod W). */
+void lorenz_ref_power_spectrum(const uint8_t* x, uint32_t H, uint32_t W, double* P) {
+  const uint64_t N = (uint64_t)H * W;
+  double* cs = (double*)malloc((size_t)(2 * N) * sizeof(double));
+  for (uint64_t t = 0; t < N; ++t) {
+    const double a = LREF_TWO_PI * (double)t / (double)N;
+    cs[2 * t] = cos(a);
+    cs[2 * t + 1] = sin(a);
+  }
+  for (uint32_t k = 0; k < H; ++k)
+    for (uint32_t l = 0; l < W; ++l)
+      P[(uint64_t)((k + H / 2) % H) * W + (l + W / 2) % W] = power_bin(x, H, W, k, l, cs);
+  free(cs);
+}
+
+/* one frequency (k,l) (unshifted indices) of the same spectrum */
+double lorenz_ref_power_at(const uint8_t* x, uint32_t H, uint32_t W, uint32_t k, uint32_t l) {
+  return power_bin(x, H, W, k, l, NULL);
+}
+
+/* Spectral flatness of a DC-centred spectrum: geometric mean / arithmetic mean of the
+ * non-DC bins. No non-DC power at all -> 0 (Q26). A zero bin makes the geometric mean 0.     */
+double lorenz_ref_spectral_flatness(const double* P, uint32_t H, uint32_t W) {
+  const uint64_t N = (uint64_t)H * W, dc = (uint64_t)(H / 2) * W + W / 2;
+  double slog = 0.0, sum = 0.0;
+  for (uint64_t i = 0; i < N; ++i) {
+    if (i == dc) continue;
+    slog += log(P[i]);
+    sum += P[i];
+  }
+  const double M = (double)(N - 1);
+  if (sum == 0.0) return 0.0;
+  return exp(slog / M) / (sum / M);
+}

@@ -113,6 +113,15 @@ int lorenz_ref_encrypt(const uint8_t* pw, size_t pw_len, const lref_params* prm,
 /* NEXT-4 analysis: Fig.1 digit histograms; hist: uint64[3*4*128], accumulated. */
 void lorenz_ref_digit_hist(const double* ic, uint64_t lanes, uint32_t skip, uint32_t samples,
                            uint32_t stride, uint32_t dt_code, uint32_t integrator, uint64_t* hist);
+/* NEXT-4 analysis, §4 Figs. 3-4 (readings Q25-Q27). x: H x W bytes, row-major.
+ * autocorr: r[u*W+v] = normalised circular 2-D autocorrelation at lag (u,v), r[0] = 1.
+ * power_spectrum: P = |DFT|^2 / (HW)^2, DC-centred (bin (k,l) at ((k+H/2)%H, (l+W/2)%W)).
+ * *_at: one lag / one (unshifted) frequency. flatness: non-DC geometric / arithmetic mean. */
+void lorenz_ref_autocorr(const uint8_t* x, uint32_t H, uint32_t W, double* r);
+double lorenz_ref_autocorr_at(const uint8_t* x, uint32_t H, uint32_t W, uint32_t u, uint32_t v);
+void lorenz_ref_power_spectrum(const uint8_t* x, uint32_t H, uint32_t W, double* P);
+double lorenz_ref_power_at(const uint8_t* x, uint32_t H, uint32_t W, uint32_t k, uint32_t l);
+double lorenz_ref_spectral_flatness(const double* P, uint32_t H, uint32_t W);
 /* One global block b of a message of length n, from that block's own bytes. */
 int lorenz_ref_encrypt_block(const uint8_t* pw, size_t pw_len, const lref_params* prm, uint64_t n,
                              uint64_t b, const uint8_t* blk_pt, uint8_t* blk_ct);
