@@ -191,6 +191,24 @@ lorenz_status lorenz_digit_histograms(const double* ic, uint64_t lanes, uint32_t
                                       uint32_t stride, uint32_t dt_code, uint32_t integrator,
                                       uint64_t* hist, void* cuda_stream);
 
+/* ---- NEXT-4 §4 analysis: Fig.3 autocorrelation matrices and Fig.4 2-D Fourier
+ * power spectra; readings Q25-Q27.
+ * x: DEVICE pointer to an H x W byte matrix, row-major (e.g. the first H*W bytes of a
+ * ciphertext); H and W powers of two in [2, 4096] (no zero padding; else LORENZ_E_ARG).
+ * Outputs are DEVICE pointers (8-aligned), written stream-ordered on `cuda_stream`; a
+ * workspace of 16*H*W bytes comes from the stream-ordered pool. FP64 FFTs: results agree
+ * with the plain-sum definitions within the bounds of DESIGN.md §2e, not bit for bit.
+ *
+ * lorenz_autocorrelation: r[u*W + v] = sum_ij d[i][j] d[(i+u)%H][(j+v)%W] / sum_ij d[i][j]^2,
+ *   d = x - mean(x) (normalised circular 2-D autocorrelation; r[0] = 1; a constant x gives
+ *   r[0] = 1 and 0 elsewhere). r must not overlap x.
+ * lorenz_power_spectrum: power[((k+H/2)%H)*W + (l+W/2)%W] = |F(k,l)|^2 / (HW)^2, F the 2-D DFT
+ *   (DC-centred; sum of power = mean(x^2)). flatness (nullable, device double): geometric /
+ *   arithmetic mean of the non-DC bins, 0 when they are all zero (deterministic reduction). */
+lorenz_status lorenz_autocorrelation(const uint8_t* x, uint32_t H, uint32_t W, double* r, void* cuda_stream);
+lorenz_status lorenz_power_spectrum(const uint8_t* x, uint32_t H, uint32_t W, double* power, double* flatness,
+                                    void* cuda_stream);
+
 /* ---- end to end from HOST buffers (the user-facing call of a file encryptor):
  * blocks [b0,b1) of an n-byte message; pt_host / ct_host are HOST pointers to the
  * slice starts (same slice convention as the device calls; [0, num_blocks) is the

@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(CSRC, "liblorenz.so")
 SOURCES = ["lorenz.cu", "lorenz_io.cu"]
-HEADERS = ["lorenz_device.cuh", "sha256.cuh", "stats.cuh", "analysis.cuh",
+HEADERS = ["lorenz_device.cuh", "sha256.cuh", "stats.cuh", "analysis.cuh", "spectra.cuh",
            os.path.join("..", "..", "include", "lorenz.h")]
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

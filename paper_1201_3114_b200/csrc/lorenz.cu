@@ -8,6 +8,7 @@
 #include <nvtx3/nvToolsExt.h>  // header-only; ranges are no-ops unless a profiler attaches
 
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -18,6 +19,7 @@
 #include "lorenz_device.cuh"
 #include "analysis.cuh"
 #include "sha256.cuh"
+#include "spectra.cuh"
 #include "stats.cuh"
 
 namespace {
@@ -552,6 +554,106 @@ lorenz_status lorenz_digit_histograms(const double* ic, uint64_t lanes, uint32_t
   else
     lz::digit_hist_kernel<LORENZ_RK4><<<grid, lz::kCta, 0, st>>>(C, ic, lanes, skip, samples, stride, h);
   return cuda_ok(cudaGetLastError(), "digit_hist") ? LORENZ_OK : LORENZ_E_CUDA;
+}
+
+// ---------------------------------------------------------------- NEXT-4 §4 spectra
+}  // extern "C"
+namespace {
+bool fft_side(uint32_t v) { return v >= 2 && v <= 4096 && (v & (v - 1)) == 0; }
+uint32_t ilog2(uint32_t v) { return 31u - (uint32_t)__builtin_clz(v); }
+
+lz::FftPass fft_rows(uint32_t H, uint32_t W) {
+  return lz::FftPass{W, ilog2(W), H, lz::fft_seq_per_cta(W, H), 1, W, H, W, 0.0};
+}
+lz::FftPass fft_cols(uint32_t H, uint32_t W) {
+  return lz::FftPass{H, ilog2(H), W, lz::fft_seq_per_cta(H, W), W, 1, H, W, 0.0};
+}
+
+template <int IN, int OUT>
+bool fft_launch(const lz::FftPass& p, const uint8_t* bytes, const double2* cin, double2* cout, double* rout,
+                const unsigned long long* sum, double* lag0, cudaStream_t st) {
+  const size_t smem = lz::fft_smem_bytes(p.n, p.C);
+  if (!cuda_ok(cudaFuncSetAttribute(lz::fft_pass_kernel<IN, OUT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem), "fft smem"))
+    return false;
+  const unsigned grid = (p.nseq + p.C - 1) / p.C;
+  lz::fft_pass_kernel<IN, OUT><<<grid, lz::kFftCta, smem, st>>>(p, bytes, cin, cout, rout, sum, lag0);
+  return cuda_ok(cudaGetLastError(), "fft pass");
+}
+
+lorenz_status spectra_args(const uint8_t* x, uint32_t H, uint32_t W, const double* out) {
+  if (!x || !out || !fft_side(H) || !fft_side(W) || (reinterpret_cast<uintptr_t>(out) & 7)) {
+    g_err = "H and W must be powers of two in [2, 4096]; x and out non-null device pointers, out 8-aligned";
+    return LORENZ_E_ARG;
+  }
+  return LORENZ_OK;
+}
+}  // namespace
+extern "C" {
+
+lorenz_status lorenz_power_spectrum(const uint8_t* x, uint32_t H, uint32_t W, double* power, double* flatness,
+                                    void* stream) {
+  Trace tr("lorenz_power_spectrum");
+  lorenz_status ret = spectra_args(x, H, W, power);
+  if (ret != LORENZ_OK) return ret;
+  cudaStream_t st = (cudaStream_t)stream;
+  keep_pool_cached();
+  const uint64_t N = (uint64_t)H * W;
+  double2* ws = nullptr;
+  double2* part = nullptr;
+  if (!cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&ws), N * sizeof(double2), st), "alloc fft"))
+    return LORENZ_E_CUDA;
+  lz::FftPass rows = fft_rows(H, W), cols = fft_cols(H, W);
+  cols.scale = std::ldexp(1.0, -2 * (int)ilog2((uint32_t)N));  // 1 / N^2
+  bool ok = fft_launch<lz::FFT_IN_BYTES, lz::FFT_OUT_COMPLEX>(rows, x, nullptr, ws, nullptr, nullptr, nullptr, st) &&
+            fft_launch<lz::FFT_IN_COMPLEX, lz::FFT_OUT_SPECTRUM>(cols, nullptr, ws, ws, power, nullptr, nullptr, st);
+  if (ok && flatness) {
+    ok = cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&part), lz::kFlatCtas * sizeof(double2), st), "alloc");
+    if (ok) {
+      lz::flatness_partial_kernel<<<lz::kFlatCtas, lz::kFftCta, 0, st>>>(power, N, (uint64_t)(H / 2) * W + W / 2,
+                                                                         part);
+      lz::flatness_final_kernel<<<1, 32, 0, st>>>(part, N - 1, flatness);
+      ok = cuda_ok(cudaGetLastError(), "flatness");
+    }
+  }
+  cudaFreeAsync(ws, st);
+  if (part) cudaFreeAsync(part, st);
+  return ok ? LORENZ_OK : LORENZ_E_CUDA;
+}
+
+lorenz_status lorenz_autocorrelation(const uint8_t* x, uint32_t H, uint32_t W, double* r, void* stream) {
+  Trace tr("lorenz_autocorrelation");
+  lorenz_status ret = spectra_args(x, H, W, r);
+  if (ret != LORENZ_OK) return ret;
+  cudaStream_t st = (cudaStream_t)stream;
+  keep_pool_cached();
+  const uint64_t N = (uint64_t)H * W;
+  double2* ws = nullptr;
+  unsigned long long* aux = nullptr;  // [0] = byte sum, [1] = lag-0 value (double bits)
+  if (!cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&ws), N * sizeof(double2), st), "alloc fft") ||
+      !cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&aux), 16, st), "alloc aux")) {
+    if (ws) cudaFreeAsync(ws, st);
+    return LORENZ_E_CUDA;
+  }
+  double* lag0 = reinterpret_cast<double*>(aux + 1);
+  const lz::FftPass rows = fft_rows(H, W), cols = fft_cols(H, W);
+  const unsigned sgrid = (unsigned)std::min<uint64_t>(4ull * sm_count(), (N + lz::kFftCta - 1) / lz::kFftCta);
+  bool ok = cuda_ok(cudaMemsetAsync(aux, 0, 16, st), "memset");
+  if (ok) {
+    lz::byte_sum_kernel<<<sgrid, lz::kFftCta, 0, st>>>(x, N, aux);
+    ok = cuda_ok(cudaGetLastError(), "byte sum") &&
+         fft_launch<lz::FFT_IN_CENTRED, lz::FFT_OUT_COMPLEX>(rows, x, nullptr, ws, nullptr, aux, nullptr, st) &&
+         fft_launch<lz::FFT_IN_COMPLEX, lz::FFT_OUT_POWER>(cols, nullptr, ws, ws, nullptr, nullptr, nullptr, st) &&
+         fft_launch<lz::FFT_IN_COMPLEX, lz::FFT_OUT_COMPLEX>(rows, nullptr, ws, ws, nullptr, nullptr, nullptr, st) &&
+         fft_launch<lz::FFT_IN_COMPLEX, lz::FFT_OUT_REAL>(cols, nullptr, ws, nullptr, r, nullptr, lag0, st);
+  }
+  if (ok) {
+    lz::autocorr_normalise_kernel<<<sgrid, lz::kFftCta, 0, st>>>(r, N, lag0);
+    ok = cuda_ok(cudaGetLastError(), "normalise");
+  }
+  cudaFreeAsync(ws, st);
+  cudaFreeAsync(aux, st);
+  return ok ? LORENZ_OK : LORENZ_E_CUDA;
 }
 
 // ---------------------------------------------------------------- C5 statistics

@@ -29,7 +29,8 @@ EXPORTS = ["lorenz_abi_version", "lorenz_last_error", "lorenz_status_string", "l
            "lorenz_encrypt_async", "lorenz_decrypt_async", "lorenz_verify_async",
            "lorenz_encrypt_batch", "lorenz_encrypt_host", "lorenz_decrypt_host",
            "lorenz_compare_spans", "lorenz_histograms", "lorenz_envelope_write", "lorenz_envelope_read",
-           "lorenz_encrypt_file", "lorenz_decrypt_file", "lorenz_digit_histograms"]
+           "lorenz_encrypt_file", "lorenz_decrypt_file", "lorenz_digit_histograms",
+           "lorenz_autocorrelation", "lorenz_power_spectrum"]
 E_IO, E_FORMAT = 7, 8
 ENVELOPE_BYTES = 24
 
@@ -99,6 +100,8 @@ def lib():
         L.lorenz_compare_spans.argtypes = [vp, vp, C.POINTER(lorenz_span), u32, vp, vp]
         L.lorenz_histograms.argtypes = [vp, C.POINTER(lorenz_span), u32, vp, vp]
         L.lorenz_digit_histograms.argtypes = [vp, u64, u32, u32, u32, u32, u32, vp, vp]
+        L.lorenz_autocorrelation.argtypes = [vp, u32, u32, vp, vp]
+        L.lorenz_power_spectrum.argtypes = [vp, u32, u32, vp, vp, vp]
         L.lorenz_envelope_write.argtypes = [kp, u64, vp]
         L.lorenz_envelope_read.argtypes = [C.c_char_p, sz, C.POINTER(lorenz_params), C.POINTER(u64),
                                            C.POINTER(u64)]
@@ -263,6 +266,21 @@ def lorenz_digit_histograms(ic, lanes: int, skip: int, samples: int, stride: int
     """Fig.1 digit histograms (NEXT-4): ic device float64 (lanes x 3), hist device int64[3*4*128]."""
     _check(lib().lorenz_digit_histograms(_ptr(ic), lanes, skip, samples, stride, dt_code, integrator, _ptr(hist),
                                          _stream(stream)), "lorenz_digit_histograms")
+
+
+def lorenz_autocorrelation(x, r, stream=None):
+    """Fig.3 (NEXT-4): x device uint8 (H, W), r device float64 (H, W) <- normalised circular 2-D
+    autocorrelation, lag (0, 0) at r[0, 0]. H, W powers of two in [2, 4096]."""
+    h, w = x.shape
+    _check(lib().lorenz_autocorrelation(_ptr(x), h, w, _ptr(r), _stream(stream)), "lorenz_autocorrelation")
+
+
+def lorenz_power_spectrum(x, power, flatness=None, stream=None):
+    """Fig.4 (NEXT-4): power device float64 (H, W) <- |DFT2(x)|^2 / (HW)^2, DC-centred;
+    flatness (device float64[1], optional) <- geometric / arithmetic mean of the non-DC bins."""
+    h, w = x.shape
+    _check(lib().lorenz_power_spectrum(_ptr(x), h, w, _ptr(power), _ptr(flatness), _stream(stream)),
+           "lorenz_power_spectrum")
 
 
 def lorenz_envelope_write(key: Key, n: int) -> bytes:
