@@ -562,23 +562,58 @@ namespace {
 bool fft_side(uint32_t v) { return v >= 2 && v <= 4096 && (v & (v - 1)) == 0; }
 uint32_t ilog2(uint32_t v) { return 31u - (uint32_t)__builtin_clz(v); }
 
-lz::FftPass fft_rows(uint32_t H, uint32_t W) {
-  return lz::FftPass{W, ilog2(W), H, lz::fft_seq_per_cta(W, H), 1, W, H, W, 0.0};
+lz::FftPass fft_rows(uint32_t H, uint32_t W, const double2* tw) {
+  lz::FftPass p = lz::fft_plan(W, ilog2(W), H, true);
+  p.stride = 1;
+  p.dist = W;
+  p.H = H;
+  p.W = W;
+  p.tw = tw;
+  return p;
 }
-lz::FftPass fft_cols(uint32_t H, uint32_t W) {
-  return lz::FftPass{H, ilog2(H), W, lz::fft_seq_per_cta(H, W), W, 1, H, W, 0.0};
+lz::FftPass fft_cols(uint32_t H, uint32_t W, const double2* tw) {
+  lz::FftPass p = lz::fft_plan(H, ilog2(H), W, false);
+  p.stride = W;
+  p.dist = 1;
+  p.H = H;
+  p.W = W;
+  p.tw = tw;
+  return p;
 }
 
 template <int IN, int OUT>
 bool fft_launch(const lz::FftPass& p, const uint8_t* bytes, const double2* cin, double2* cout, double* rout,
                 const unsigned long long* sum, double* lag0, cudaStream_t st) {
-  const size_t smem = lz::fft_smem_bytes(p.n, p.C);
-  if (!cuda_ok(cudaFuncSetAttribute(lz::fft_pass_kernel<IN, OUT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)smem), "fft smem"))
-    return false;
-  const unsigned grid = (p.nseq + p.C - 1) / p.C;
-  lz::fft_pass_kernel<IN, OUT><<<grid, lz::kFftCta, smem, st>>>(p, bytes, cin, cout, rout, sum, lag0);
-  return cuda_ok(cudaGetLastError(), "fft pass");
+  const size_t smem = lz::fft_smem_bytes(p);
+  const unsigned grid = (p.nseq + p.S - 1) / p.S;
+  auto go = [&](auto kernel) {
+    if (!cuda_ok(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "fft smem"))
+      return false;
+    kernel<<<grid, lz::fft_cta(p.n, p.stride == 1), smem, st>>>(p, bytes, cin, cout, rout, sum, lag0);
+    return cuda_ok(cudaGetLastError(), "fft pass");
+  };
+  switch (p.logn) {
+    case 1: return go(lz::fft_pass_kernel<IN, OUT, 1, 256>);
+    case 2: return go(lz::fft_pass_kernel<IN, OUT, 2, 256>);
+    case 3: return go(lz::fft_pass_kernel<IN, OUT, 3, 256>);
+    case 4: return go(lz::fft_pass_kernel<IN, OUT, 4, 256>);
+    case 5: return go(lz::fft_pass_kernel<IN, OUT, 5, 256>);
+    case 6: return go(lz::fft_pass_kernel<IN, OUT, 6, 256>);
+    case 7: return go(lz::fft_pass_kernel<IN, OUT, 7, 256>);
+    case 8: return go(lz::fft_pass_kernel<IN, OUT, 8, 256>);
+    case 9: return go(lz::fft_pass_kernel<IN, OUT, 9, 256>);
+    case 10: return go(lz::fft_pass_kernel<IN, OUT, 10, 256>);
+    case 11: return go(lz::fft_pass_kernel<IN, OUT, 11, 256>);
+    default:
+      return p.stride == 1 ? go(lz::fft_pass_kernel<IN, OUT, 12, 256>) : go(lz::fft_pass_kernel<IN, OUT, 12, 512>);
+  }
+}
+
+// twiddle tables for the row (W) and column (H) lengths: tw[0..W) then tw[W..W+H)
+bool fft_twiddles(double2* tw, uint32_t H, uint32_t W, cudaStream_t st) {
+  lz::twiddle_kernel<<<(W + 255) / 256, 256, 0, st>>>(tw, W);
+  lz::twiddle_kernel<<<(H + 255) / 256, 256, 0, st>>>(tw + W, H);
+  return cuda_ok(cudaGetLastError(), "twiddles");
 }
 
 lorenz_status spectra_args(const uint8_t* x, uint32_t H, uint32_t W, const double* out) {
@@ -601,20 +636,21 @@ lorenz_status lorenz_power_spectrum(const uint8_t* x, uint32_t H, uint32_t W, do
   const uint64_t N = (uint64_t)H * W;
   double2* ws = nullptr;
   double2* part = nullptr;
-  if (!cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&ws), N * sizeof(double2), st), "alloc fft"))
+  if (!cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&ws), (N + H + W) * sizeof(double2), st), "alloc fft"))
     return LORENZ_E_CUDA;
-  lz::FftPass rows = fft_rows(H, W), cols = fft_cols(H, W);
+  double2* tw = ws + N;
+  lz::FftPass rows = fft_rows(H, W, tw), cols = fft_cols(H, W, tw + W);
   cols.scale = std::ldexp(1.0, -2 * (int)ilog2((uint32_t)N));  // 1 / N^2
-  bool ok = fft_launch<lz::FFT_IN_BYTES, lz::FFT_OUT_COMPLEX>(rows, x, nullptr, ws, nullptr, nullptr, nullptr, st) &&
-            fft_launch<lz::FFT_IN_COMPLEX, lz::FFT_OUT_SPECTRUM>(cols, nullptr, ws, ws, power, nullptr, nullptr, st);
+  const uint32_t nparts = (cols.nseq + cols.S - 1) / cols.S;  // one flatness partial per column CTA
+  bool ok = !flatness ||
+            cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&part), nparts * sizeof(double2), st), "alloc");
+  cols.part = flatness ? part : nullptr;
+  ok = ok && fft_twiddles(tw, H, W, st) &&
+       fft_launch<lz::FFT_IN_BYTES, lz::FFT_OUT_COMPLEX>(rows, x, nullptr, ws, nullptr, nullptr, nullptr, st) &&
+       fft_launch<lz::FFT_IN_COMPLEX, lz::FFT_OUT_SPECTRUM>(cols, nullptr, ws, ws, power, nullptr, nullptr, st);
   if (ok && flatness) {
-    ok = cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&part), lz::kFlatCtas * sizeof(double2), st), "alloc");
-    if (ok) {
-      lz::flatness_partial_kernel<<<lz::kFlatCtas, lz::kFftCta, 0, st>>>(power, N, (uint64_t)(H / 2) * W + W / 2,
-                                                                         part);
-      lz::flatness_final_kernel<<<1, 32, 0, st>>>(part, N - 1, flatness);
-      ok = cuda_ok(cudaGetLastError(), "flatness");
-    }
+    lz::flatness_final_kernel<<<1, 32, 0, st>>>(part, nparts, N - 1, flatness);
+    ok = cuda_ok(cudaGetLastError(), "flatness");
   }
   cudaFreeAsync(ws, st);
   if (part) cudaFreeAsync(part, st);
@@ -630,15 +666,16 @@ lorenz_status lorenz_autocorrelation(const uint8_t* x, uint32_t H, uint32_t W, d
   const uint64_t N = (uint64_t)H * W;
   double2* ws = nullptr;
   unsigned long long* aux = nullptr;  // [0] = byte sum, [1] = lag-0 value (double bits)
-  if (!cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&ws), N * sizeof(double2), st), "alloc fft") ||
+  if (!cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&ws), (N + H + W) * sizeof(double2), st), "alloc fft") ||
       !cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&aux), 16, st), "alloc aux")) {
     if (ws) cudaFreeAsync(ws, st);
     return LORENZ_E_CUDA;
   }
   double* lag0 = reinterpret_cast<double*>(aux + 1);
-  const lz::FftPass rows = fft_rows(H, W), cols = fft_cols(H, W);
+  double2* tw = ws + N;
+  const lz::FftPass rows = fft_rows(H, W, tw), cols = fft_cols(H, W, tw + W);
   const unsigned sgrid = (unsigned)std::min<uint64_t>(4ull * sm_count(), (N + lz::kFftCta - 1) / lz::kFftCta);
-  bool ok = cuda_ok(cudaMemsetAsync(aux, 0, 16, st), "memset");
+  bool ok = cuda_ok(cudaMemsetAsync(aux, 0, 16, st), "memset") && fft_twiddles(tw, H, W, st);
   if (ok) {
     lz::byte_sum_kernel<<<sgrid, lz::kFftCta, 0, st>>>(x, N, aux);
     ok = cuda_ok(cudaGetLastError(), "byte sum") &&

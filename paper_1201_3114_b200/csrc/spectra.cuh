@@ -7,112 +7,255 @@
 //   autocorrelation r = Re FFT2(|FFT2(x - mean)|^2) / (its lag-0 value)   (Wiener-Khinchin;
 //                   FFT instead of the inverse FFT: the input is real, so only a conjugation
 //                   differs and Re is unchanged).
-// One pass = one batch of 1-D FFTs of length n along rows (stride 1) or columns (stride W):
-// a CTA loads C sequences into shared memory in bit-reversed order (coalesced along the
-// contiguous axis), runs the log2(n) radix-2 DIT stages in place against a per-CTA
-// twiddle table (sincospi of exact dyadic arguments), and writes back through a fused epilogue
-// (|F|^2, the DC shift and 1/N^2 scaling, or the real part). HBM / shared-memory bound:
-// 5 log2(n) flops per element per pass against 32 bytes of HBM traffic.
+// One pass = one batch of 1-D FFTs of length n = 2^L along rows (stride 1) or columns
+// (stride W), as Stockham autosort radix-16 passes (the last one radix 2^(L mod 4) when L is
+// not a multiple of 4) held in registers: each thread owns 16 elements (n >= 16) or a whole
+// sequence (n < 16). The first pass reads HBM directly (coalesced along the contiguous axis),
+// the last pass writes HBM directly through a fused epilogue (|F|^2, the DC shift and 1/N^2
+// scaling, or the real part); between passes the tile is exchanged through shared memory
+// (padded by one element per 16 against bank conflicts). Twiddles exp(-2 pi i m / n) come from
+// a per-call table (sincospi of exact dyadic arguments, L1/L2-resident); the in-register
+// 2..16-point DFTs use compile-time constants. At n = 4096: 3 passes, 2 exchanges.
+// HBM-bound: 16 B read + 16 B written per element per 1-D pass (bytes / doubles at the ends).
 #pragma once
 #include <cstdint>
 
 namespace lz {
 
-constexpr int kFftCta = 256;
-constexpr uint32_t kFftElems = 4096;  // complex elements per CTA (64 KiB + padding + twiddles)
+constexpr int kFftCtaThreads = 256;
 
 enum FftIn : int { FFT_IN_BYTES = 0, FFT_IN_CENTRED = 1, FFT_IN_COMPLEX = 2 };
 enum FftOut : int { FFT_OUT_COMPLEX = 0, FFT_OUT_POWER = 1, FFT_OUT_SPECTRUM = 2, FFT_OUT_REAL = 3 };
 
 struct FftPass {
-  uint32_t n, logn;   // FFT length (power of two) and log2(n)
-  uint32_t nseq, C;   // sequences in the batch, sequences per CTA
-  uint64_t stride;    // elements between consecutive points of a sequence (1 = rows)
-  uint64_t dist;      // elements between consecutive sequences
-  uint32_t H, W;      // matrix shape (for the DC shift)
-  double scale;       // FFT_OUT_SPECTRUM: 1 / (HW)^2 (a power of two: exact)
+  uint32_t n, logn;     // FFT length (power of two, 2..4096) and log2(n)
+  uint32_t nseq;        // sequences in the batch
+  uint32_t T, S;        // threads per sequence (n/16, or 1 when n < 16), sequences per CTA
+  uint32_t pitch;       // shared-memory elements per sequence (n + n/16)
+  uint32_t npass;       // Stockham passes
+  uint32_t rlog[4];     // log2 of each pass's radix
+  uint64_t stride;      // elements between consecutive points of a sequence (1 = rows)
+  uint64_t dist;        // elements between consecutive sequences
+  uint32_t H, W;        // matrix shape (for the DC shift)
+  double scale;         // FFT_OUT_SPECTRUM: 1 / (HW)^2 (a power of two: exact)
+  const double2* tw;    // exp(-2 pi i m / n), m < n
+  double2* part;        // FFT_OUT_SPECTRUM (nullable): per-CTA (sum log P, sum P) over non-DC bins
 };
 
-__host__ __device__ inline uint32_t fft_seq_per_cta(uint32_t n, uint32_t nseq) {
-  const uint32_t c = n >= kFftElems ? 1u : kFftElems / n;
-  return c < nseq ? c : nseq;
+// CTA threads: 256, except 512 for 4096-point column passes (S = 2 adjacent columns per CTA,
+// so every 32-byte sector a warp touches is fully used)
+inline uint32_t fft_cta(uint32_t n, bool rows) { return (!rows && n >= 4096) ? 512 : 256; }
+
+inline FftPass fft_plan(uint32_t n, uint32_t logn, uint32_t nseq, bool rows) {
+  FftPass p{};
+  p.n = n;
+  p.logn = logn;
+  p.nseq = nseq;
+  p.T = n >= 16 ? n / 16 : 1;
+  const uint32_t S = fft_cta(n, rows) / p.T;
+  p.S = S < nseq ? S : nseq;
+  p.pitch = n + n / 16;
+  p.npass = 0;
+  uint32_t L = logn;
+  while (L >= 4) { p.rlog[p.npass++] = 4; L -= 4; }
+  if (L) p.rlog[p.npass++] = L;
+  return p;
 }
-__host__ __device__ inline size_t fft_smem_bytes(uint32_t n, uint32_t C) {
-  return (size_t)C * (n + 1) * 16 + (size_t)(n / 2) * 16;  // padded sequences + twiddles
+inline size_t fft_smem_bytes(const FftPass& p) {
+  return p.npass > 1 ? (size_t)p.S * p.pitch * 16 : 0;
 }
 
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(__dadd_rn(a.x, b.x), __dadd_rn(a.y, b.y)); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(__dsub_rn(a.x, b.x), __dsub_rn(a.y, b.y)); }
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
   return make_double2(__dsub_rn(__dmul_rn(a.x, b.x), __dmul_rn(a.y, b.y)),
                       __dadd_rn(__dmul_rn(a.x, b.y), __dmul_rn(a.y, b.x)));
 }
 
-// element e of the CTA's tile -> (sequence s in the CTA, point k): the contiguous axis is the
-// fastest-varying thread index, so global loads / stores coalesce along rows or along columns
-__device__ __forceinline__ void fft_map(const FftPass& p, uint32_t e, uint32_t& s, uint32_t& k) {
-  if (p.stride == 1) { s = e >> p.logn; k = e & (p.n - 1); }
-  else { s = e % p.C; k = e / p.C; }
+// x * exp(-2 pi i m / 16), m a compile-time constant after unrolling: 1 and -i are free
+__device__ __forceinline__ double2 rot16(double2 x, int m) {
+  constexpr double C1 = 0.92387953251128673848, C2 = 0.70710678118654752440, C3 = 0.38268343236508978178;
+  switch (m) {
+    case 0: return x;
+    case 4: return make_double2(x.y, -x.x);
+    case 2: return make_double2(__dmul_rn(__dadd_rn(x.x, x.y), C2), __dmul_rn(__dsub_rn(x.y, x.x), C2));
+    case 6: return make_double2(__dmul_rn(__dsub_rn(x.y, x.x), C2), __dmul_rn(-__dadd_rn(x.x, x.y), C2));
+    case 1: return cmul(x, make_double2(C1, -C3));
+    case 3: return cmul(x, make_double2(C3, -C1));
+    case 5: return cmul(x, make_double2(-C3, -C1));
+    default: return cmul(x, make_double2(-C1, -C3));  // 7
+  }
 }
 
-template <int IN, int OUT>
-__global__ void __launch_bounds__(kFftCta)
+// in-register R-point DFT (decimation in frequency): y_u lands in a[O + bitrev_R(u)]
+template <int R>
+__device__ __forceinline__ void dft_dif(double2 (&a)[16], const int O) {  // O: constant after unrolling
+#pragma unroll
+  for (int h = R / 2; h >= 1; h >>= 1)
+#pragma unroll
+    for (int b = 0; b < R; b += 2 * h)
+#pragma unroll
+      for (int j = 0; j < h; ++j) {
+        const double2 u = a[O + b + j], v = a[O + b + j + h];
+        a[O + b + j] = cadd(u, v);
+        a[O + b + j + h] = rot16(csub(u, v), j * (16 / (2 * h)));
+      }
+}
+
+template <int R>
+__device__ __forceinline__ int bitrev_c(int u) {
+  int r = 0;
+#pragma unroll
+  for (int b = 1; b < R; b <<= 1) r = (r << 1) | ((u & b) ? 1 : 0);
+  return r;
+}
+
+__device__ __forceinline__ uint32_t fft_pad(uint32_t i) { return i + (i >> 4); }
+
+template <int IN>
+__device__ __forceinline__ double2 fft_load(const FftPass& p, uint64_t seq, uint32_t idx, const uint8_t* bytes,
+                                            const double2* cin, double mean) {
+  const uint64_t g = seq * p.dist + (uint64_t)idx * p.stride;
+  if (IN == FFT_IN_COMPLEX) return cin[g];
+  if (IN == FFT_IN_CENTRED) return make_double2(__dsub_rn((double)bytes[g], mean), 0.0);  // exact (HW = 2^k)
+  return make_double2((double)bytes[g], 0.0);
+}
+
+template <int OUT>
+__device__ __forceinline__ void fft_store(const FftPass& p, uint64_t seq, uint32_t pos, double2 v, double2* cout,
+                                          double* rout, double* lag0, double2& acc) {
+  const uint64_t g = seq * p.dist + (uint64_t)pos * p.stride;
+  if (OUT == FFT_OUT_COMPLEX) {
+    cout[g] = v;
+  } else if (OUT == FFT_OUT_POWER) {
+    cout[g] = make_double2(__dadd_rn(__dmul_rn(v.x, v.x), __dmul_rn(v.y, v.y)), 0.0);
+  } else if (OUT == FFT_OUT_SPECTRUM) {
+    const uint64_t i = g / p.W, j = g % p.W;  // frequency (k, l) -> DC-centred position
+    const uint64_t o = ((i + p.H / 2) & (p.H - 1)) * p.W + ((j + p.W / 2) & (p.W - 1));
+    const double P = __dmul_rn(__dadd_rn(__dmul_rn(v.x, v.x), __dmul_rn(v.y, v.y)), p.scale);
+    rout[o] = P;
+    if (p.part && g != 0) acc = make_double2(__dadd_rn(acc.x, log(P)), __dadd_rn(acc.y, P));  // flatness
+  } else {
+    rout[g] = v.x;
+    if (g == 0) *lag0 = v.x;
+  }
+}
+
+// one Stockham pass of radix R after sub-transforms of length LS: group j (< N/R) takes
+// x[j + t N/R], t < R, multiplies by exp(-2 pi i t k / (LS R)), k = j mod LS, does the R-point
+// DFT and writes y_u to (j - k) R + k + u LS. Everything but the thread's indices is static.
+template <int R, int N, int LS, bool FIRST, bool LAST, int IN, int OUT>
+__device__ __forceinline__ void fft_pass(const FftPass& p, double2 (&a)[16], double2* Xs, uint32_t tid, uint64_t seq,
+                                         bool active, bool valid, const uint8_t* bytes, const double2* cin,
+                                         double2* cout, double* rout, double* lag0, double mean, double2& acc) {
+  constexpr int E = N < 16 ? N : 16, G = E / R, T = N / E, NR = N / R;
+#pragma unroll
+  for (int g = 0; g < G && active; ++g) {
+    const uint32_t j = tid + g * T;
+#pragma unroll
+    for (int t = 0; t < R; ++t) {
+      const uint32_t idx = j + t * NR;
+      if (FIRST) a[g * R + t] = valid ? fft_load<IN>(p, seq, idx, bytes, cin, mean) : make_double2(0.0, 0.0);
+      else a[g * R + t] = Xs[fft_pad(idx)];
+    }
+  }
+  if (!FIRST) __syncthreads();  // every read of this pass done before anyone overwrites the tile
+#pragma unroll
+  for (int g = 0; g < G && active; ++g) {
+    const uint32_t j = tid + g * T, k = j & (LS - 1);
+    if (LS > 1 && k) {
+      // w^t for t < R from the table entries w, w^2, w^4, w^8 only: w^t = w^(t&3) * w^(t&12)
+      // (at most two extra complex products per factor)
+      const uint32_t step = k * (N / (LS * R));
+      const double2 one = make_double2(1.0, 0.0);
+      const double2 w1 = __ldg(p.tw + step);
+      const double2 w2 = R > 2 ? __ldg(p.tw + 2 * step) : one;
+      const double2 w3 = R > 2 ? cmul(w1, w2) : one;
+      const double2 w4 = R > 4 ? __ldg(p.tw + 4 * step) : one;
+      const double2 w8 = R > 8 ? __ldg(p.tw + 8 * step) : one;
+      const double2 w12 = R > 8 ? cmul(w4, w8) : one;
+#pragma unroll
+      for (int t = 1; t < R; ++t) {
+        const int lo = t & 3, hi = t & 12;
+        const double2 wl = lo == 1 ? w1 : lo == 2 ? w2 : w3;
+        const double2 wh = hi == 4 ? w4 : hi == 8 ? w8 : w12;
+        const double2 w = lo == 0 ? wh : hi == 0 ? wl : cmul(wl, wh);
+        a[g * R + t] = cmul(a[g * R + t], w);
+      }
+    }
+    dft_dif<R>(a, g * R);
+#pragma unroll
+    for (int u = 0; u < R; ++u) {
+      const uint32_t pos = (j - k) * R + k + u * LS;
+      const double2 v = a[g * R + bitrev_c<R>(u)];
+      if (LAST) {
+        if (valid) fft_store<OUT>(p, seq, pos, v, cout, rout, lag0, acc);
+      } else {
+        Xs[fft_pad(pos)] = v;
+      }
+    }
+  }
+  if (!LAST) __syncthreads();
+}
+
+// the passes of an N = 2^LOGN transform: radix 16 while >= 4 bits remain, then the remainder
+template <int LOGN, int DONE, int IN, int OUT>
+__device__ __forceinline__ void fft_passes(const FftPass& p, double2 (&a)[16], double2* Xs, uint32_t tid, uint64_t seq,
+                                           bool active, bool valid, const uint8_t* bytes, const double2* cin,
+                                           double2* cout, double* rout, double* lag0, double mean, double2& acc) {
+  constexpr int REM = LOGN - DONE, RL = REM >= 4 ? 4 : REM;
+  fft_pass<1 << RL, 1 << LOGN, 1 << DONE, DONE == 0, REM == RL, IN, OUT>(p, a, Xs, tid, seq, active, valid, bytes,
+                                                                          cin, cout, rout, lag0, mean, acc);
+  if constexpr (REM > RL)
+    fft_passes<LOGN, DONE + RL, IN, OUT>(p, a, Xs, tid, seq, active, valid, bytes, cin, cout, rout, lag0, mean, acc);
+}
+
+// CTA = 256 threads = S sequences x T = N/16 threads (T = 1 when N < 16); rows: a sequence's
+// threads are adjacent; columns: adjacent threads take adjacent columns (coalescing)
+template <int IN, int OUT, int LOGN, int CTA>
+__global__ void __launch_bounds__(CTA, 512 / CTA)
     fft_pass_kernel(const FftPass p, const uint8_t* __restrict__ bytes, const double2* cin, double2* cout,
                     double* __restrict__ rout, const unsigned long long* __restrict__ sum, double* __restrict__ lag0) {
+  constexpr int N = 1 << LOGN, T = N < 16 ? 1 : N / 16;
   extern __shared__ double2 fsm[];
-  double2* tw = fsm + (size_t)p.C * (p.n + 1);
-  const uint32_t n = p.n, half = n >> 1, row = n + 1;
-  const uint64_t seq0 = (uint64_t)blockIdx.x * p.C;
-  const uint32_t C = (seq0 + p.C <= p.nseq) ? p.C : (uint32_t)(p.nseq - seq0);
-  for (uint32_t t = threadIdx.x; t < half; t += kFftCta) {  // exp(-2 pi i t / n)
-    double s, c;
-    sincospi(__ddiv_rn(2.0 * t, (double)n), &s, &c);
-    tw[t] = make_double2(c, -s);
-  }
+  uint32_t s, tid;
+  if (p.stride == 1) { s = threadIdx.x / T; tid = threadIdx.x % T; }
+  else { s = threadIdx.x % p.S; tid = threadIdx.x / p.S; }
+  const uint64_t seq = (uint64_t)blockIdx.x * p.S + s;
+  const bool active = s < p.S && tid < (uint32_t)T;  // (a CTA narrower than 256 threads leaves some idle)
+  const bool valid = active && seq < p.nseq;
+  double2* Xs = fsm + (size_t)(active ? s : 0) * p.pitch;
   double mean = 0.0;
-  if (IN == FFT_IN_CENTRED) mean = __ddiv_rn((double)*sum, (double)p.H * (double)p.W);  // exact: HW = 2^k
-  const uint32_t E = C * n;
-  for (uint32_t e = threadIdx.x; e < E; e += kFftCta) {
-    uint32_t s, k;
-    fft_map(p, e, s, k);
-    const uint64_t g = (seq0 + s) * p.dist + (uint64_t)k * p.stride;
-    double2 v;
-    if (IN == FFT_IN_COMPLEX) v = cin[g];
-    else if (IN == FFT_IN_CENTRED) v = make_double2(__dsub_rn((double)bytes[g], mean), 0.0);  // exact
-    else v = make_double2((double)bytes[g], 0.0);
-    fsm[s * row + (__brev(k) >> (32 - p.logn))] = v;
-  }
-  __syncthreads();
-  // radix-2 DIT, in place; stage with half-size m uses twiddle index j * (n / 2m)
-  for (uint32_t lm = 0; lm < p.logn; ++lm) {
-    const uint32_t m = 1u << lm, tshift = p.logn - 1 - lm;
-    for (uint32_t b = threadIdx.x; b < C * half; b += kFftCta) {
-      const uint32_t s = b >> (p.logn - 1), q = b & (half - 1);
-      const uint32_t j = q & (m - 1), i0 = ((q >> lm) << (lm + 1)) + j;
-      double2* xs = fsm + s * row;
-      const double2 a = xs[i0], t = cmul(tw[j << tshift], xs[i0 + m]);
-      xs[i0] = make_double2(__dadd_rn(a.x, t.x), __dadd_rn(a.y, t.y));
-      xs[i0 + m] = make_double2(__dsub_rn(a.x, t.x), __dsub_rn(a.y, t.y));
-    }
+  if (IN == FFT_IN_CENTRED) mean = __ddiv_rn((double)*sum, (double)p.H * (double)p.W);
+  double2 a[16];
+  double2 acc = make_double2(0.0, 0.0);
+  fft_passes<LOGN, 0, IN, OUT>(p, a, Xs, tid, seq, active, valid, bytes, cin, cout, rout, lag0, mean, acc);
+  if (OUT == FFT_OUT_SPECTRUM && p.part) {  // fused flatness partials: fixed order -> deterministic
+    __shared__ double2 red[CTA / 32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+      acc = make_double2(__dadd_rn(acc.x, __shfl_xor_sync(0xffffffffu, acc.x, o)),
+                         __dadd_rn(acc.y, __shfl_xor_sync(0xffffffffu, acc.y, o)));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
     __syncthreads();
-  }
-  for (uint32_t e = threadIdx.x; e < E; e += kFftCta) {
-    uint32_t s, k;
-    fft_map(p, e, s, k);
-    const uint64_t g = (seq0 + s) * p.dist + (uint64_t)k * p.stride;
-    const double2 v = fsm[s * row + k];
-    if (OUT == FFT_OUT_COMPLEX) {
-      cout[g] = v;
-    } else if (OUT == FFT_OUT_POWER) {
-      cout[g] = make_double2(__dadd_rn(__dmul_rn(v.x, v.x), __dmul_rn(v.y, v.y)), 0.0);
-    } else if (OUT == FFT_OUT_SPECTRUM) {
-      const uint64_t i = g / p.W, jj = g % p.W;  // frequency (k, l) -> DC-centred position
-      const uint64_t o = ((i + p.H / 2) & (p.H - 1)) * p.W + ((jj + p.W / 2) & (p.W - 1));
-      rout[o] = __dmul_rn(__dadd_rn(__dmul_rn(v.x, v.x), __dmul_rn(v.y, v.y)), p.scale);
-    } else {
-      rout[g] = v.x;
-      if (g == 0) *lag0 = v.x;
+    if (threadIdx.x == 0) {
+      double2 t = red[0];
+      for (int w = 1; w < CTA / 32; ++w) t = make_double2(__dadd_rn(t.x, red[w].x), __dadd_rn(t.y, red[w].y));
+      p.part[blockIdx.x] = t;
     }
   }
 }
+
+// twiddle table exp(-2 pi i m / n), m < n
+__global__ void twiddle_kernel(double2* __restrict__ tw, uint32_t n) {
+  const uint32_t m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= n) return;
+  double s, c;
+  sincospi(__ddiv_rn(2.0 * m, (double)n), &s, &c);
+  tw[m] = make_double2(c, -s);
+}
+
+constexpr int kFftCta = 256;  // the reductions below
 
 // sum of the H*W bytes (the mean of the autocorrelation's centring; < 2^36, exact)
 __global__ void __launch_bounds__(kFftCta) byte_sum_kernel(const uint8_t* __restrict__ x, uint64_t n,
@@ -133,37 +276,13 @@ __global__ void __launch_bounds__(kFftCta) autocorr_normalise_kernel(double* __r
     r[i] = c0 == 0.0 ? (i == 0 ? 1.0 : 0.0) : __ddiv_rn(r[i], c0);
 }
 
-// spectral flatness of a DC-centred spectrum: per-CTA partial (sum log P, sum P) over the non-DC
-// bins in a fixed grid-stride order, then one CTA combines the partials in index order
-// (deterministic: the same bits every run)
-constexpr int kFlatCtas = 296;
-__global__ void __launch_bounds__(kFftCta) flatness_partial_kernel(const double* __restrict__ P, uint64_t n,
-                                                                   uint64_t dc, double2* __restrict__ part) {
-  __shared__ double2 red[kFftCta / 32];
-  double sl = 0.0, sp = 0.0;
-  for (uint64_t i = (uint64_t)blockIdx.x * kFftCta + threadIdx.x; i < n; i += (uint64_t)kFlatCtas * kFftCta)
-    if (i != dc) {
-      sl = __dadd_rn(sl, log(P[i]));
-      sp = __dadd_rn(sp, P[i]);
-    }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    sl = __dadd_rn(sl, __shfl_xor_sync(0xffffffffu, sl, o));
-    sp = __dadd_rn(sp, __shfl_xor_sync(0xffffffffu, sp, o));
-  }
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = make_double2(sl, sp);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double2 a = red[0];
-    for (int w = 1; w < kFftCta / 32; ++w) a = make_double2(__dadd_rn(a.x, red[w].x), __dadd_rn(a.y, red[w].y));
-    part[blockIdx.x] = a;
-  }
-}
-
-__global__ void flatness_final_kernel(const double2* __restrict__ part, uint64_t bins, double* __restrict__ out) {
+// spectral flatness = exp(mean log P) / mean P over the non-DC bins, from the per-CTA partials
+// of the spectrum's column pass, combined in index order (deterministic: same bits every run)
+__global__ void flatness_final_kernel(const double2* __restrict__ part, uint32_t nparts, uint64_t bins,
+                                      double* __restrict__ out) {
   if (threadIdx.x) return;
   double sl = 0.0, sp = 0.0;
-  for (int b = 0; b < kFlatCtas; ++b) {
+  for (uint32_t b = 0; b < nparts; ++b) {
     sl = __dadd_rn(sl, part[b].x);
     sp = __dadd_rn(sp, part[b].y);
   }
