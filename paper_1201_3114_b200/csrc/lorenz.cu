@@ -649,7 +649,7 @@ lorenz_status lorenz_power_spectrum(const uint8_t* x, uint32_t H, uint32_t W, do
        fft_launch<lz::FFT_IN_BYTES, lz::FFT_OUT_COMPLEX>(rows, x, nullptr, ws, nullptr, nullptr, nullptr, st) &&
        fft_launch<lz::FFT_IN_COMPLEX, lz::FFT_OUT_SPECTRUM>(cols, nullptr, ws, ws, power, nullptr, nullptr, st);
   if (ok && flatness) {
-    lz::flatness_final_kernel<<<1, 32, 0, st>>>(part, nparts, N - 1, flatness);
+    lz::flatness_final_kernel<<<1, lz::kFftCta, 0, st>>>(part, nparts, N - 1, flatness);
     ok = cuda_ok(cudaGetLastError(), "flatness");
   }
   cudaFreeAsync(ws, st);

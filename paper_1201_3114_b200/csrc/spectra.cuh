@@ -112,32 +112,60 @@ __device__ __forceinline__ int bitrev_c(int u) {
 
 __device__ __forceinline__ uint32_t fft_pad(uint32_t i) { return i + (i >> 4); }
 
-template <int IN>
-__device__ __forceinline__ double2 fft_load(const FftPass& p, uint64_t seq, uint32_t idx, const uint8_t* bytes,
-                                            const double2* cin, double mean) {
-  const uint64_t g = seq * p.dist + (uint64_t)idx * p.stride;
-  if (IN == FFT_IN_COMPLEX) return cin[g];
-  if (IN == FFT_IN_CENTRED) return make_double2(__dsub_rn((double)bytes[g], mean), 0.0);  // exact (HW = 2^k)
-  return make_double2((double)bytes[g], 0.0);
+// flatness accumulator of one thread: sum P, and sum log P kept as a product of frexp mantissas
+// (each in [1/2, 1): at most 16 per thread, so no underflow) plus an exponent sum -> one log per
+// thread instead of one per bin
+struct FlatAcc {
+  double sp = 0.0, mprod = 1.0;
+  int esum = 0;
+  __device__ __forceinline__ void add(double P) {
+    int e;
+    const double m = frexp(P, &e);  // P = m 2^e; P = 0 -> m = 0 (log -> -inf: geometric mean 0)
+    mprod = __dmul_rn(mprod, m);
+    esum += e;
+    sp = __dadd_rn(sp, P);
+  }
+  __device__ __forceinline__ double sum_log() const {
+    return __dadd_rn(log(mprod), __dmul_rn((double)esum, 0.69314718055994530942));
+  }
+};
+
+// the kernel's operands and per-CTA constants
+struct FftIo {
+  const uint8_t* bytes;  // FFT_IN_BYTES / FFT_IN_CENTRED input (global)
+  const uint8_t* sb;     // the same bytes staged in shared memory (row passes), or null
+  uint64_t seq0;         // first sequence of the CTA (index origin of sb)
+  const double2* cin;
+  double2* cout;
+  double* rout;
+  double* lag0;
+  double mean;
+};
+
+template <int IN, int N>
+__device__ __forceinline__ double2 fft_load(const FftPass& p, const FftIo& io, uint64_t seq, uint32_t idx) {
+  if (IN == FFT_IN_COMPLEX) return io.cin[seq * p.dist + (uint64_t)idx * p.stride];
+  const double b = io.sb ? (double)io.sb[(seq - io.seq0) * N + idx] : (double)io.bytes[seq * p.dist + (uint64_t)idx * p.stride];
+  return make_double2(IN == FFT_IN_CENTRED ? __dsub_rn(b, io.mean) : b, 0.0);  // exact (HW = 2^k)
 }
 
 template <int OUT>
-__device__ __forceinline__ void fft_store(const FftPass& p, uint64_t seq, uint32_t pos, double2 v, double2* cout,
-                                          double* rout, double* lag0, double2& acc) {
+__device__ __forceinline__ void fft_store(const FftPass& p, const FftIo& io, uint64_t seq, uint32_t pos, double2 v,
+                                          FlatAcc& acc) {
   const uint64_t g = seq * p.dist + (uint64_t)pos * p.stride;
   if (OUT == FFT_OUT_COMPLEX) {
-    cout[g] = v;
+    io.cout[g] = v;
   } else if (OUT == FFT_OUT_POWER) {
-    cout[g] = make_double2(__dadd_rn(__dmul_rn(v.x, v.x), __dmul_rn(v.y, v.y)), 0.0);
+    io.cout[g] = make_double2(__dadd_rn(__dmul_rn(v.x, v.x), __dmul_rn(v.y, v.y)), 0.0);
   } else if (OUT == FFT_OUT_SPECTRUM) {
     const uint64_t i = g / p.W, j = g % p.W;  // frequency (k, l) -> DC-centred position
     const uint64_t o = ((i + p.H / 2) & (p.H - 1)) * p.W + ((j + p.W / 2) & (p.W - 1));
     const double P = __dmul_rn(__dadd_rn(__dmul_rn(v.x, v.x), __dmul_rn(v.y, v.y)), p.scale);
-    rout[o] = P;
-    if (p.part && g != 0) acc = make_double2(__dadd_rn(acc.x, log(P)), __dadd_rn(acc.y, P));  // flatness
+    io.rout[o] = P;
+    if (p.part && g != 0) acc.add(P);  // flatness over the non-DC bins
   } else {
-    rout[g] = v.x;
-    if (g == 0) *lag0 = v.x;
+    io.rout[g] = v.x;
+    if (g == 0) *io.lag0 = v.x;
   }
 }
 
@@ -145,9 +173,8 @@ __device__ __forceinline__ void fft_store(const FftPass& p, uint64_t seq, uint32
 // x[j + t N/R], t < R, multiplies by exp(-2 pi i t k / (LS R)), k = j mod LS, does the R-point
 // DFT and writes y_u to (j - k) R + k + u LS. Everything but the thread's indices is static.
 template <int R, int N, int LS, bool FIRST, bool LAST, int IN, int OUT>
-__device__ __forceinline__ void fft_pass(const FftPass& p, double2 (&a)[16], double2* Xs, uint32_t tid, uint64_t seq,
-                                         bool active, bool valid, const uint8_t* bytes, const double2* cin,
-                                         double2* cout, double* rout, double* lag0, double mean, double2& acc) {
+__device__ __forceinline__ void fft_pass(const FftPass& p, const FftIo& io, double2 (&a)[16], double2* Xs,
+                                         uint32_t tid, uint64_t seq, bool active, bool valid, FlatAcc& acc) {
   constexpr int E = N < 16 ? N : 16, G = E / R, T = N / E, NR = N / R;
 #pragma unroll
   for (int g = 0; g < G && active; ++g) {
@@ -155,7 +182,7 @@ __device__ __forceinline__ void fft_pass(const FftPass& p, double2 (&a)[16], dou
 #pragma unroll
     for (int t = 0; t < R; ++t) {
       const uint32_t idx = j + t * NR;
-      if (FIRST) a[g * R + t] = valid ? fft_load<IN>(p, seq, idx, bytes, cin, mean) : make_double2(0.0, 0.0);
+      if (FIRST) a[g * R + t] = valid ? fft_load<IN, N>(p, io, seq, idx) : make_double2(0.0, 0.0);
       else a[g * R + t] = Xs[fft_pad(idx)];
     }
   }
@@ -189,7 +216,7 @@ __device__ __forceinline__ void fft_pass(const FftPass& p, double2 (&a)[16], dou
       const uint32_t pos = (j - k) * R + k + u * LS;
       const double2 v = a[g * R + bitrev_c<R>(u)];
       if (LAST) {
-        if (valid) fft_store<OUT>(p, seq, pos, v, cout, rout, lag0, acc);
+        if (valid) fft_store<OUT>(p, io, seq, pos, v, acc);
       } else {
         Xs[fft_pad(pos)] = v;
       }
@@ -200,18 +227,16 @@ __device__ __forceinline__ void fft_pass(const FftPass& p, double2 (&a)[16], dou
 
 // the passes of an N = 2^LOGN transform: radix 16 while >= 4 bits remain, then the remainder
 template <int LOGN, int DONE, int IN, int OUT>
-__device__ __forceinline__ void fft_passes(const FftPass& p, double2 (&a)[16], double2* Xs, uint32_t tid, uint64_t seq,
-                                           bool active, bool valid, const uint8_t* bytes, const double2* cin,
-                                           double2* cout, double* rout, double* lag0, double mean, double2& acc) {
+__device__ __forceinline__ void fft_passes(const FftPass& p, const FftIo& io, double2 (&a)[16], double2* Xs,
+                                           uint32_t tid, uint64_t seq, bool active, bool valid, FlatAcc& acc) {
   constexpr int REM = LOGN - DONE, RL = REM >= 4 ? 4 : REM;
-  fft_pass<1 << RL, 1 << LOGN, 1 << DONE, DONE == 0, REM == RL, IN, OUT>(p, a, Xs, tid, seq, active, valid, bytes,
-                                                                          cin, cout, rout, lag0, mean, acc);
-  if constexpr (REM > RL)
-    fft_passes<LOGN, DONE + RL, IN, OUT>(p, a, Xs, tid, seq, active, valid, bytes, cin, cout, rout, lag0, mean, acc);
+  fft_pass<1 << RL, 1 << LOGN, 1 << DONE, DONE == 0, REM == RL, IN, OUT>(p, io, a, Xs, tid, seq, active, valid, acc);
+  if constexpr (REM > RL) fft_passes<LOGN, DONE + RL, IN, OUT>(p, io, a, Xs, tid, seq, active, valid, acc);
 }
 
-// CTA = 256 threads = S sequences x T = N/16 threads (T = 1 when N < 16); rows: a sequence's
-// threads are adjacent; columns: adjacent threads take adjacent columns (coalescing)
+// CTA = S sequences x T = N/16 threads (T = 1 when N < 16); rows: a sequence's threads are
+// adjacent; columns: adjacent threads take adjacent columns (coalescing). Byte-input row passes
+// first stage the CTA's rows (S N = 4096 bytes) in shared memory with one 16-byte load per thread.
 template <int IN, int OUT, int LOGN, int CTA>
 __global__ void __launch_bounds__(CTA, 512 / CTA)
     fft_pass_kernel(const FftPass p, const uint8_t* __restrict__ bytes, const double2* cin, double2* cout,
@@ -221,17 +246,28 @@ __global__ void __launch_bounds__(CTA, 512 / CTA)
   uint32_t s, tid;
   if (p.stride == 1) { s = threadIdx.x / T; tid = threadIdx.x % T; }
   else { s = threadIdx.x % p.S; tid = threadIdx.x / p.S; }
-  const uint64_t seq = (uint64_t)blockIdx.x * p.S + s;
+  const uint64_t seq0 = (uint64_t)blockIdx.x * p.S, seq = seq0 + s;
   const bool active = s < p.S && tid < (uint32_t)T;  // (a CTA narrower than 256 threads leaves some idle)
   const bool valid = active && seq < p.nseq;
   double2* Xs = fsm + (size_t)(active ? s : 0) * p.pitch;
-  double mean = 0.0;
-  if (IN == FFT_IN_CENTRED) mean = __ddiv_rn((double)*sum, (double)p.H * (double)p.W);
+  FftIo io{bytes, nullptr, seq0, cin, cout, rout, lag0, 0.0};
+  if (IN == FFT_IN_CENTRED) io.mean = __ddiv_rn((double)*sum, (double)p.H * (double)p.W);
+  if constexpr (IN != FFT_IN_COMPLEX && N >= 16 && CTA == 256) {
+    __shared__ uint4 stage[CTA];  // S N = CTA * 16 bytes
+    if (p.stride == 1 && (reinterpret_cast<uintptr_t>(bytes) & 15) == 0) {
+      const uint64_t rows = (p.nseq - seq0 < p.S) ? p.nseq - seq0 : p.S;
+      if ((uint64_t)threadIdx.x * 16 < rows * N)
+        stage[threadIdx.x] = __ldg(reinterpret_cast<const uint4*>(bytes + seq0 * N) + threadIdx.x);
+      __syncthreads();
+      io.sb = reinterpret_cast<const uint8_t*>(stage);
+    }
+  }
   double2 a[16];
-  double2 acc = make_double2(0.0, 0.0);
-  fft_passes<LOGN, 0, IN, OUT>(p, a, Xs, tid, seq, active, valid, bytes, cin, cout, rout, lag0, mean, acc);
+  FlatAcc fa;
+  fft_passes<LOGN, 0, IN, OUT>(p, io, a, Xs, tid, seq, active, valid, fa);
   if (OUT == FFT_OUT_SPECTRUM && p.part) {  // fused flatness partials: fixed order -> deterministic
     __shared__ double2 red[CTA / 32];
+    double2 acc = make_double2(fa.sum_log(), fa.sp);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1)
       acc = make_double2(__dadd_rn(acc.x, __shfl_xor_sync(0xffffffffu, acc.x, o)),
@@ -278,16 +314,26 @@ __global__ void __launch_bounds__(kFftCta) autocorr_normalise_kernel(double* __r
 
 // spectral flatness = exp(mean log P) / mean P over the non-DC bins, from the per-CTA partials
 // of the spectrum's column pass, combined in index order (deterministic: same bits every run)
-__global__ void flatness_final_kernel(const double2* __restrict__ part, uint32_t nparts, uint64_t bins,
-                                      double* __restrict__ out) {
-  if (threadIdx.x) return;
+__global__ void __launch_bounds__(kFftCta) flatness_final_kernel(const double2* __restrict__ part, uint32_t nparts,
+                                                                 uint64_t bins, double* __restrict__ out) {
+  __shared__ double2 red[kFftCta];
   double sl = 0.0, sp = 0.0;
-  for (uint32_t b = 0; b < nparts; ++b) {
+  for (uint32_t b = threadIdx.x; b < nparts; b += kFftCta) {  // fixed assignment and order
     sl = __dadd_rn(sl, part[b].x);
     sp = __dadd_rn(sp, part[b].y);
   }
-  const double M = (double)bins;
-  *out = sp == 0.0 ? 0.0 : __ddiv_rn(exp(__ddiv_rn(sl, M)), __ddiv_rn(sp, M));
+  red[threadIdx.x] = make_double2(sl, sp);
+  __syncthreads();
+  for (int h = kFftCta / 2; h > 0; h >>= 1) {
+    if ((int)threadIdx.x < h)
+      red[threadIdx.x] = make_double2(__dadd_rn(red[threadIdx.x].x, red[threadIdx.x + h].x),
+                                      __dadd_rn(red[threadIdx.x].y, red[threadIdx.x + h].y));
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double M = (double)bins;
+    *out = red[0].y == 0.0 ? 0.0 : __ddiv_rn(exp(__ddiv_rn(red[0].x, M)), __ddiv_rn(red[0].y, M));
+  }
 }
 
 }  // namespace lz
