@@ -562,19 +562,25 @@ namespace {
 bool fft_side(uint32_t v) { return v >= 2 && v <= 4096 && (v & (v - 1)) == 0; }
 uint32_t ilog2(uint32_t v) { return 31u - (uint32_t)__builtin_clz(v); }
 
-lz::FftPass fft_rows(uint32_t H, uint32_t W, const double2* tw) {
+// workspace row pitch (elements). Padding it (2..256 elements) measured no difference at 4096^2,
+// so the workspace is dense.
+uint64_t fft_ws_pitch(uint32_t W) { return W; }
+
+lz::FftPass fft_rows(uint32_t H, uint32_t W, const double2* tw, uint64_t in_pitch, uint64_t out_pitch) {
   lz::FftPass p = lz::fft_plan(W, ilog2(W), H, true);
-  p.stride = 1;
-  p.dist = W;
+  p.rows = 1;
+  p.in_pitch = in_pitch;
+  p.out_pitch = out_pitch;
   p.H = H;
   p.W = W;
   p.tw = tw;
   return p;
 }
-lz::FftPass fft_cols(uint32_t H, uint32_t W, const double2* tw) {
+lz::FftPass fft_cols(uint32_t H, uint32_t W, const double2* tw, uint64_t in_pitch, uint64_t out_pitch) {
   lz::FftPass p = lz::fft_plan(H, ilog2(H), W, false);
-  p.stride = W;
-  p.dist = 1;
+  p.rows = 0;
+  p.in_pitch = in_pitch;
+  p.out_pitch = out_pitch;
   p.H = H;
   p.W = W;
   p.tw = tw;
@@ -589,7 +595,7 @@ bool fft_launch(const lz::FftPass& p, const uint8_t* bytes, const double2* cin, 
   auto go = [&](auto kernel) {
     if (!cuda_ok(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "fft smem"))
       return false;
-    kernel<<<grid, lz::fft_cta(p.n, p.stride == 1), smem, st>>>(p, bytes, cin, cout, rout, sum, lag0);
+    kernel<<<grid, lz::fft_cta(p.n, p.rows != 0), smem, st>>>(p, bytes, cin, cout, rout, sum, lag0);
     return cuda_ok(cudaGetLastError(), "fft pass");
   };
   switch (p.logn) {
@@ -605,7 +611,8 @@ bool fft_launch(const lz::FftPass& p, const uint8_t* bytes, const double2* cin, 
     case 10: return go(lz::fft_pass_kernel<IN, OUT, 10, 256>);
     case 11: return go(lz::fft_pass_kernel<IN, OUT, 11, 256>);
     default:
-      return p.stride == 1 ? go(lz::fft_pass_kernel<IN, OUT, 12, 256>) : go(lz::fft_pass_kernel<IN, OUT, 12, 512>);
+      return lz::fft_cta(p.n, p.rows != 0) == 256 ? go(lz::fft_pass_kernel<IN, OUT, 12, 256>)
+                                                     : go(lz::fft_pass_kernel<IN, OUT, 12, 512>);
   }
 }
 
@@ -636,10 +643,11 @@ lorenz_status lorenz_power_spectrum(const uint8_t* x, uint32_t H, uint32_t W, do
   const uint64_t N = (uint64_t)H * W;
   double2* ws = nullptr;
   double2* part = nullptr;
-  if (!cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&ws), (N + H + W) * sizeof(double2), st), "alloc fft"))
+  const uint64_t Pw = fft_ws_pitch(W), NW = (uint64_t)H * Pw;
+  if (!cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&ws), (NW + H + W) * sizeof(double2), st), "alloc fft"))
     return LORENZ_E_CUDA;
-  double2* tw = ws + N;
-  lz::FftPass rows = fft_rows(H, W, tw), cols = fft_cols(H, W, tw + W);
+  double2* tw = ws + NW;
+  lz::FftPass rows = fft_rows(H, W, tw, W, Pw), cols = fft_cols(H, W, tw + W, Pw, W);
   cols.scale = std::ldexp(1.0, -2 * (int)ilog2((uint32_t)N));  // 1 / N^2
   const uint32_t nparts = (cols.nseq + cols.S - 1) / cols.S;  // one flatness partial per column CTA
   bool ok = !flatness ||
@@ -666,23 +674,25 @@ lorenz_status lorenz_autocorrelation(const uint8_t* x, uint32_t H, uint32_t W, d
   const uint64_t N = (uint64_t)H * W;
   double2* ws = nullptr;
   unsigned long long* aux = nullptr;  // [0] = byte sum, [1] = lag-0 value (double bits)
-  if (!cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&ws), (N + H + W) * sizeof(double2), st), "alloc fft") ||
+  const uint64_t Pw = fft_ws_pitch(W), NW = (uint64_t)H * Pw;
+  if (!cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&ws), (NW + H + W) * sizeof(double2), st), "alloc fft") ||
       !cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&aux), 16, st), "alloc aux")) {
     if (ws) cudaFreeAsync(ws, st);
     return LORENZ_E_CUDA;
   }
   double* lag0 = reinterpret_cast<double*>(aux + 1);
-  double2* tw = ws + N;
-  const lz::FftPass rows = fft_rows(H, W, tw), cols = fft_cols(H, W, tw + W);
+  double2* tw = ws + NW;
+  const lz::FftPass rows1 = fft_rows(H, W, tw, W, Pw), cols1 = fft_cols(H, W, tw + W, Pw, Pw);
+  const lz::FftPass rows2 = fft_rows(H, W, tw, Pw, Pw), cols2 = fft_cols(H, W, tw + W, Pw, W);
   const unsigned sgrid = (unsigned)std::min<uint64_t>(4ull * sm_count(), (N + lz::kFftCta - 1) / lz::kFftCta);
   bool ok = cuda_ok(cudaMemsetAsync(aux, 0, 16, st), "memset") && fft_twiddles(tw, H, W, st);
   if (ok) {
     lz::byte_sum_kernel<<<sgrid, lz::kFftCta, 0, st>>>(x, N, aux);
     ok = cuda_ok(cudaGetLastError(), "byte sum") &&
-         fft_launch<lz::FFT_IN_CENTRED, lz::FFT_OUT_COMPLEX>(rows, x, nullptr, ws, nullptr, aux, nullptr, st) &&
-         fft_launch<lz::FFT_IN_COMPLEX, lz::FFT_OUT_POWER>(cols, nullptr, ws, ws, nullptr, nullptr, nullptr, st) &&
-         fft_launch<lz::FFT_IN_COMPLEX, lz::FFT_OUT_COMPLEX>(rows, nullptr, ws, ws, nullptr, nullptr, nullptr, st) &&
-         fft_launch<lz::FFT_IN_COMPLEX, lz::FFT_OUT_REAL>(cols, nullptr, ws, nullptr, r, nullptr, lag0, st);
+         fft_launch<lz::FFT_IN_CENTRED, lz::FFT_OUT_COMPLEX>(rows1, x, nullptr, ws, nullptr, aux, nullptr, st) &&
+         fft_launch<lz::FFT_IN_COMPLEX, lz::FFT_OUT_POWER>(cols1, nullptr, ws, ws, nullptr, nullptr, nullptr, st) &&
+         fft_launch<lz::FFT_IN_COMPLEX, lz::FFT_OUT_COMPLEX>(rows2, nullptr, ws, ws, nullptr, nullptr, nullptr, st) &&
+         fft_launch<lz::FFT_IN_COMPLEX, lz::FFT_OUT_REAL>(cols2, nullptr, ws, nullptr, r, nullptr, lag0, st);
   }
   if (ok) {
     lz::autocorr_normalise_kernel<<<sgrid, lz::kFftCta, 0, st>>>(r, N, lag0);

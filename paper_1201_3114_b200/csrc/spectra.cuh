@@ -34,8 +34,9 @@ struct FftPass {
   uint32_t pitch;       // shared-memory elements per sequence (n + n/16)
   uint32_t npass;       // Stockham passes
   uint32_t rlog[4];     // log2 of each pass's radix
-  uint64_t stride;      // elements between consecutive points of a sequence (1 = rows)
-  uint64_t dist;        // elements between consecutive sequences
+  uint32_t rows;        // 1: sequences are rows (element (seq, idx)); 0: columns (element (idx, seq))
+  uint64_t in_pitch;    // row pitch (elements) of the input matrix
+  uint64_t out_pitch;   // row pitch of a complex (workspace) output
   uint32_t H, W;        // matrix shape (for the DC shift)
   double scale;         // FFT_OUT_SPECTRUM: 1 / (HW)^2 (a power of two: exact)
   const double2* tw;    // exp(-2 pi i m / n), m < n
@@ -140,32 +141,41 @@ struct FftIo {
   double* rout;
   double* lag0;
   double mean;
+  const double2* tlo;    // shared: exp(-2 pi i m / n), m < 64
+  const double2* thi;    // shared: exp(-2 pi i 64 m / n), m < n / 64
 };
+
+// exp(-2 pi i m / n) = tlo[m mod 64] * thi[m / 64] (n <= 4096: two 64-entry shared tables)
+template <int N>
+__device__ __forceinline__ double2 twid(const FftIo& io, uint32_t m) {
+  if (N <= 64) return io.tlo[m];
+  return cmul(io.tlo[m & 63], io.thi[m >> 6]);
+}
 
 template <int IN, int N>
 __device__ __forceinline__ double2 fft_load(const FftPass& p, const FftIo& io, uint64_t seq, uint32_t idx) {
-  if (IN == FFT_IN_COMPLEX) return io.cin[seq * p.dist + (uint64_t)idx * p.stride];
-  const double b = io.sb ? (double)io.sb[(seq - io.seq0) * N + idx] : (double)io.bytes[seq * p.dist + (uint64_t)idx * p.stride];
+  const uint64_t g = p.rows ? seq * p.in_pitch + idx : (uint64_t)idx * p.in_pitch + seq;
+  if (IN == FFT_IN_COMPLEX) return io.cin[g];
+  const double b = io.sb ? (double)io.sb[(seq - io.seq0) * N + idx] : (double)io.bytes[g];
   return make_double2(IN == FFT_IN_CENTRED ? __dsub_rn(b, io.mean) : b, 0.0);  // exact (HW = 2^k)
 }
 
 template <int OUT>
 __device__ __forceinline__ void fft_store(const FftPass& p, const FftIo& io, uint64_t seq, uint32_t pos, double2 v,
                                           FlatAcc& acc) {
-  const uint64_t g = seq * p.dist + (uint64_t)pos * p.stride;
+  const uint64_t i = p.rows ? seq : pos, j = p.rows ? pos : seq;  // (row, column) of the element
   if (OUT == FFT_OUT_COMPLEX) {
-    io.cout[g] = v;
+    io.cout[i * p.out_pitch + j] = v;
   } else if (OUT == FFT_OUT_POWER) {
-    io.cout[g] = make_double2(__dadd_rn(__dmul_rn(v.x, v.x), __dmul_rn(v.y, v.y)), 0.0);
-  } else if (OUT == FFT_OUT_SPECTRUM) {
-    const uint64_t i = g / p.W, j = g % p.W;  // frequency (k, l) -> DC-centred position
+    io.cout[i * p.out_pitch + j] = make_double2(__dadd_rn(__dmul_rn(v.x, v.x), __dmul_rn(v.y, v.y)), 0.0);
+  } else if (OUT == FFT_OUT_SPECTRUM) {  // frequency (k, l) = (i, j) -> DC-centred position
     const uint64_t o = ((i + p.H / 2) & (p.H - 1)) * p.W + ((j + p.W / 2) & (p.W - 1));
     const double P = __dmul_rn(__dadd_rn(__dmul_rn(v.x, v.x), __dmul_rn(v.y, v.y)), p.scale);
     io.rout[o] = P;
-    if (p.part && g != 0) acc.add(P);  // flatness over the non-DC bins
+    if (p.part && (i | j) != 0) acc.add(P);  // flatness over the non-DC bins
   } else {
-    io.rout[g] = v.x;
-    if (g == 0) *io.lag0 = v.x;
+    io.rout[i * p.W + j] = v.x;
+    if ((i | j) == 0) *io.lag0 = v.x;
   }
 }
 
@@ -191,15 +201,15 @@ __device__ __forceinline__ void fft_pass(const FftPass& p, const FftIo& io, doub
   for (int g = 0; g < G && active; ++g) {
     const uint32_t j = tid + g * T, k = j & (LS - 1);
     if (LS > 1 && k) {
-      // w^t for t < R from the table entries w, w^2, w^4, w^8 only: w^t = w^(t&3) * w^(t&12)
-      // (at most two extra complex products per factor)
+      // w^t for t < R from w, w^2, w^4, w^8 only: w^t = w^(t&3) * w^(t&12) (at most two extra
+      // complex products per factor); each w^(2^i) is itself a product of two shared-table entries
       const uint32_t step = k * (N / (LS * R));
       const double2 one = make_double2(1.0, 0.0);
-      const double2 w1 = __ldg(p.tw + step);
-      const double2 w2 = R > 2 ? __ldg(p.tw + 2 * step) : one;
+      const double2 w1 = twid<N>(io, step);
+      const double2 w2 = R > 2 ? twid<N>(io, 2 * step) : one;
       const double2 w3 = R > 2 ? cmul(w1, w2) : one;
-      const double2 w4 = R > 4 ? __ldg(p.tw + 4 * step) : one;
-      const double2 w8 = R > 8 ? __ldg(p.tw + 8 * step) : one;
+      const double2 w4 = R > 4 ? twid<N>(io, 4 * step) : one;
+      const double2 w8 = R > 8 ? twid<N>(io, 8 * step) : one;
       const double2 w12 = R > 8 ? cmul(w4, w8) : one;
 #pragma unroll
       for (int t = 1; t < R; ++t) {
@@ -244,24 +254,28 @@ __global__ void __launch_bounds__(CTA, 512 / CTA)
   constexpr int N = 1 << LOGN, T = N < 16 ? 1 : N / 16;
   extern __shared__ double2 fsm[];
   uint32_t s, tid;
-  if (p.stride == 1) { s = threadIdx.x / T; tid = threadIdx.x % T; }
+  if (p.rows) { s = threadIdx.x / T; tid = threadIdx.x % T; }
   else { s = threadIdx.x % p.S; tid = threadIdx.x / p.S; }
   const uint64_t seq0 = (uint64_t)blockIdx.x * p.S, seq = seq0 + s;
   const bool active = s < p.S && tid < (uint32_t)T;  // (a CTA narrower than 256 threads leaves some idle)
   const bool valid = active && seq < p.nseq;
   double2* Xs = fsm + (size_t)(active ? s : 0) * p.pitch;
-  FftIo io{bytes, nullptr, seq0, cin, cout, rout, lag0, 0.0};
+  __shared__ double2 tws[64 + (N > 64 ? N / 64 : 1)];
+  for (uint32_t i = threadIdx.x; i < 64 + (N > 64 ? N / 64 : 0); i += CTA)
+    if (i < 64) { if (i < (uint32_t)N) tws[i] = __ldg(p.tw + i); }
+    else tws[i] = __ldg(p.tw + 64 * (i - 64));
+  FftIo io{bytes, nullptr, seq0, cin, cout, rout, lag0, 0.0, tws, tws + 64};
   if (IN == FFT_IN_CENTRED) io.mean = __ddiv_rn((double)*sum, (double)p.H * (double)p.W);
   if constexpr (IN != FFT_IN_COMPLEX && N >= 16 && CTA == 256) {
     __shared__ uint4 stage[CTA];  // S N = CTA * 16 bytes
-    if (p.stride == 1 && (reinterpret_cast<uintptr_t>(bytes) & 15) == 0) {
+    if (p.rows && p.in_pitch == N && (reinterpret_cast<uintptr_t>(bytes) & 15) == 0) {
       const uint64_t rows = (p.nseq - seq0 < p.S) ? p.nseq - seq0 : p.S;
       if ((uint64_t)threadIdx.x * 16 < rows * N)
         stage[threadIdx.x] = __ldg(reinterpret_cast<const uint4*>(bytes + seq0 * N) + threadIdx.x);
-      __syncthreads();
       io.sb = reinterpret_cast<const uint8_t*>(stage);
     }
   }
+  __syncthreads();  // twiddle tables (and the staged bytes) visible to the CTA
   double2 a[16];
   FlatAcc fa;
   fft_passes<LOGN, 0, IN, OUT>(p, io, a, Xs, tid, seq, active, valid, fa);
