@@ -587,15 +587,27 @@ lz::FftPass fft_cols(uint32_t H, uint32_t W, const double2* tw, uint64_t in_pitc
   return p;
 }
 
+// one 1-D FFT pass over the batch; n >= 1024 runs the persistent prefetching kernel (complex input,
+// or 16-byte aligned byte rows). *grid_out = the grid used (one flatness partial per CTA).
 template <int IN, int OUT>
 bool fft_launch(const lz::FftPass& p, const uint8_t* bytes, const double2* cin, double2* cout, double* rout,
-                const unsigned long long* sum, double* lag0, cudaStream_t st) {
+                const unsigned long long* sum, double* lag0, cudaStream_t st, unsigned* grid_out = nullptr) {
   const size_t smem = lz::fft_smem_bytes(p);
-  const unsigned grid = (p.nseq + p.S - 1) / p.S;
+  const unsigned tiles = (p.nseq + p.S - 1) / p.S, cta = lz::fft_cta(p.n, p.rows != 0);
+  const bool persist =
+      p.logn >= 10 && (IN == lz::FFT_IN_COMPLEX || (p.rows && p.in_pitch == p.n && aligned16(bytes)));
   auto go = [&](auto kernel) {
     if (!cuda_ok(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "fft smem"))
       return false;
-    kernel<<<grid, lz::fft_cta(p.n, p.rows != 0), smem, st>>>(p, bytes, cin, cout, rout, sum, lag0);
+    unsigned grid = tiles;
+    if (persist) {
+      int occ = 0;
+      if (!cuda_ok(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, (int)cta, smem), "fft occupancy"))
+        return false;
+      grid = std::min<unsigned>(tiles, (unsigned)std::max(1, occ) * (unsigned)sm_count());
+    }
+    if (grid_out) *grid_out = grid;
+    kernel<<<grid, cta, smem, st>>>(p, bytes, cin, cout, rout, sum, lag0);
     return cuda_ok(cudaGetLastError(), "fft pass");
   };
   switch (p.logn) {
@@ -608,11 +620,14 @@ bool fft_launch(const lz::FftPass& p, const uint8_t* bytes, const double2* cin, 
     case 7: return go(lz::fft_pass_kernel<IN, OUT, 7, 256>);
     case 8: return go(lz::fft_pass_kernel<IN, OUT, 8, 256>);
     case 9: return go(lz::fft_pass_kernel<IN, OUT, 9, 256>);
-    case 10: return go(lz::fft_pass_kernel<IN, OUT, 10, 256>);
-    case 11: return go(lz::fft_pass_kernel<IN, OUT, 11, 256>);
+    case 10:
+      return persist ? go(lz::fft_persistent_kernel<IN, OUT, 10, 256>) : go(lz::fft_pass_kernel<IN, OUT, 10, 256>);
+    case 11:
+      return persist ? go(lz::fft_persistent_kernel<IN, OUT, 11, 256>) : go(lz::fft_pass_kernel<IN, OUT, 11, 256>);
     default:
-      return lz::fft_cta(p.n, p.rows != 0) == 256 ? go(lz::fft_pass_kernel<IN, OUT, 12, 256>)
-                                                     : go(lz::fft_pass_kernel<IN, OUT, 12, 512>);
+      if (cta == 512)
+        return persist ? go(lz::fft_persistent_kernel<IN, OUT, 12, 512>) : go(lz::fft_pass_kernel<IN, OUT, 12, 512>);
+      return persist ? go(lz::fft_persistent_kernel<IN, OUT, 12, 256>) : go(lz::fft_pass_kernel<IN, OUT, 12, 256>);
   }
 }
 
@@ -649,13 +664,15 @@ lorenz_status lorenz_power_spectrum(const uint8_t* x, uint32_t H, uint32_t W, do
   double2* tw = ws + NW;
   lz::FftPass rows = fft_rows(H, W, tw, W, Pw), cols = fft_cols(H, W, tw + W, Pw, W);
   cols.scale = std::ldexp(1.0, -2 * (int)ilog2((uint32_t)N));  // 1 / N^2
-  const uint32_t nparts = (cols.nseq + cols.S - 1) / cols.S;  // one flatness partial per column CTA
+  const uint32_t tiles = (cols.nseq + cols.S - 1) / cols.S;  // >= the column pass's grid
+  unsigned nparts = 0;                                          // one flatness partial per column CTA
   bool ok = !flatness ||
-            cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&part), nparts * sizeof(double2), st), "alloc");
+            cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&part), tiles * sizeof(double2), st), "alloc");
   cols.part = flatness ? part : nullptr;
   ok = ok && fft_twiddles(tw, H, W, st) &&
        fft_launch<lz::FFT_IN_BYTES, lz::FFT_OUT_COMPLEX>(rows, x, nullptr, ws, nullptr, nullptr, nullptr, st) &&
-       fft_launch<lz::FFT_IN_COMPLEX, lz::FFT_OUT_SPECTRUM>(cols, nullptr, ws, ws, power, nullptr, nullptr, st);
+       fft_launch<lz::FFT_IN_COMPLEX, lz::FFT_OUT_SPECTRUM>(cols, nullptr, ws, ws, power, nullptr, nullptr, st,
+                                                            &nparts);
   if (ok && flatness) {
     lz::flatness_final_kernel<<<1, lz::kFftCta, 0, st>>>(part, nparts, N - 1, flatness);
     ok = cuda_ok(cudaGetLastError(), "flatness");

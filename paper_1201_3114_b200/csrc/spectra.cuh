@@ -31,6 +31,7 @@ struct FftPass {
   uint32_t n, logn;     // FFT length (power of two, 2..4096) and log2(n)
   uint32_t nseq;        // sequences in the batch
   uint32_t T, S;        // threads per sequence (n/16, or 1 when n < 16), sequences per CTA
+  uint32_t logS;        // log2(S) (S is a power of two)
   uint32_t pitch;       // shared-memory elements per sequence (n + n/16)
   uint32_t npass;       // Stockham passes
   uint32_t rlog[4];     // log2 of each pass's radix
@@ -55,7 +56,14 @@ inline FftPass fft_plan(uint32_t n, uint32_t logn, uint32_t nseq, bool rows) {
   p.T = n >= 16 ? n / 16 : 1;
   const uint32_t S = fft_cta(n, rows) / p.T;
   p.S = S < nseq ? S : nseq;
+  p.logS = 0;
+  while ((1u << p.logS) < p.S) ++p.logS;
+  // shared pitch: the padded sequence (+1 per 16) plus an offset that puts the k sequences an
+  // 8-thread shared-memory phase touches (k = 8/T rows, or min(8, S) columns) 128/k bytes apart,
+  // so the phase's 16-byte accesses fall in distinct bank groups
+  const uint32_t k = rows ? (p.T >= 8 ? 1 : 8 / p.T) : (p.S < 8 ? p.S : 8);
   p.pitch = n + n / 16;
+  if (k > 1) p.pitch += ((8 / k) - p.pitch % 8 + 8) % 8;  // pitch = 8/k (mod 8)
   p.npass = 0;
   uint32_t L = logn;
   while (L >= 4) { p.rlog[p.npass++] = 4; L -= 4; }
@@ -120,8 +128,18 @@ struct FlatAcc {
   double sp = 0.0, mprod = 1.0;
   int esum = 0;
   __device__ __forceinline__ void add(double P) {
+    // P = m 2^e, m in [1/2, 1): exponent field split off with integer ops for normal P >= 0;
+    // zero and subnormals take frexp (P = 0 -> m = 0: log -> -inf, geometric mean 0)
+    const long long b = __double_as_longlong(P);
+    const int ef = (int)(b >> 52) & 0x7ff;
+    double m;
     int e;
-    const double m = frexp(P, &e);  // P = m 2^e; P = 0 -> m = 0 (log -> -inf: geometric mean 0)
+    if (ef != 0) {
+      m = __longlong_as_double((b & 0x800fffffffffffffLL) | 0x3fe0000000000000LL);
+      e = ef - 1022;
+    } else {
+      m = frexp(P, &e);
+    }
     mprod = __dmul_rn(mprod, m);
     esum += e;
     sp = __dadd_rn(sp, P);
@@ -182,21 +200,27 @@ __device__ __forceinline__ void fft_store(const FftPass& p, const FftIo& io, uin
 // one Stockham pass of radix R after sub-transforms of length LS: group j (< N/R) takes
 // x[j + t N/R], t < R, multiplies by exp(-2 pi i t k / (LS R)), k = j mod LS, does the R-point
 // DFT and writes y_u to (j - k) R + k + u LS. Everything but the thread's indices is static.
-template <int R, int N, int LS, bool FIRST, bool LAST, int IN, int OUT>
+// SMEM_SRC: the first pass reads a tile already prefetched into Xs (complex input) or the byte
+// stage; `pre` is called by every thread of the last pass once the tile is no longer read (the
+// persistent kernel prefetches its next tile there, overlapping the last pass and its stores).
+template <int R, int N, int LS, bool FIRST, bool LAST, int IN, int OUT, bool SMEM_SRC, typename Pre>
 __device__ __forceinline__ void fft_pass(const FftPass& p, const FftIo& io, double2 (&a)[16], double2* Xs,
-                                         uint32_t tid, uint64_t seq, bool active, bool valid, FlatAcc& acc) {
+                                         uint32_t tid, uint64_t seq, bool active, bool valid, FlatAcc& acc,
+                                         const Pre& pre) {
   constexpr int E = N < 16 ? N : 16, G = E / R, T = N / E, NR = N / R;
+  constexpr bool FROM_XS = !FIRST || (SMEM_SRC && IN == FFT_IN_COMPLEX);
 #pragma unroll
   for (int g = 0; g < G && active; ++g) {
     const uint32_t j = tid + g * T;
 #pragma unroll
     for (int t = 0; t < R; ++t) {
       const uint32_t idx = j + t * NR;
-      if (FIRST) a[g * R + t] = valid ? fft_load<IN, N>(p, io, seq, idx) : make_double2(0.0, 0.0);
+      if (!FROM_XS) a[g * R + t] = valid ? fft_load<IN, N>(p, io, seq, idx) : make_double2(0.0, 0.0);
       else a[g * R + t] = Xs[fft_pad(idx)];
     }
   }
-  if (!FIRST) __syncthreads();  // every read of this pass done before anyone overwrites the tile
+  if (FROM_XS) __syncthreads();  // every read of this pass done before anyone overwrites the tile
+  if (LAST) pre();
 #pragma unroll
   for (int g = 0; g < G && active; ++g) {
     const uint32_t j = tid + g * T, k = j & (LS - 1);
@@ -236,12 +260,37 @@ __device__ __forceinline__ void fft_pass(const FftPass& p, const FftIo& io, doub
 }
 
 // the passes of an N = 2^LOGN transform: radix 16 while >= 4 bits remain, then the remainder
-template <int LOGN, int DONE, int IN, int OUT>
+template <int LOGN, int DONE, int IN, int OUT, bool SMEM_SRC = false, typename Pre = void (*)()>
 __device__ __forceinline__ void fft_passes(const FftPass& p, const FftIo& io, double2 (&a)[16], double2* Xs,
-                                           uint32_t tid, uint64_t seq, bool active, bool valid, FlatAcc& acc) {
+                                           uint32_t tid, uint64_t seq, bool active, bool valid, FlatAcc& acc,
+                                           const Pre& pre) {
   constexpr int REM = LOGN - DONE, RL = REM >= 4 ? 4 : REM;
-  fft_pass<1 << RL, 1 << LOGN, 1 << DONE, DONE == 0, REM == RL, IN, OUT>(p, io, a, Xs, tid, seq, active, valid, acc);
-  if constexpr (REM > RL) fft_passes<LOGN, DONE + RL, IN, OUT>(p, io, a, Xs, tid, seq, active, valid, acc);
+  fft_pass<1 << RL, 1 << LOGN, 1 << DONE, DONE == 0, REM == RL, IN, OUT, SMEM_SRC>(p, io, a, Xs, tid, seq, active,
+                                                                                    valid, acc, pre);
+  if constexpr (REM > RL)
+    fft_passes<LOGN, DONE + RL, IN, OUT, SMEM_SRC>(p, io, a, Xs, tid, seq, active, valid, acc, pre);
+}
+
+__device__ __forceinline__ void no_prefetch() {}
+
+// per-CTA flatness partial (sum log P, sum P): warp shuffles then warps in order (deterministic)
+template <int CTA>
+__device__ __forceinline__ void flat_partial(const FlatAcc& fa, double2* part) {
+  {
+    __shared__ double2 red[CTA / 32];
+    double2 acc = make_double2(fa.sum_log(), fa.sp);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+      acc = make_double2(__dadd_rn(acc.x, __shfl_xor_sync(0xffffffffu, acc.x, o)),
+                         __dadd_rn(acc.y, __shfl_xor_sync(0xffffffffu, acc.y, o)));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double2 t = red[0];
+      for (int w = 1; w < CTA / 32; ++w) t = make_double2(__dadd_rn(t.x, red[w].x), __dadd_rn(t.y, red[w].y));
+      part[blockIdx.x] = t;
+    }
+  }
 }
 
 // CTA = S sequences x T = N/16 threads (T = 1 when N < 16); rows: a sequence's threads are
@@ -255,7 +304,7 @@ __global__ void __launch_bounds__(CTA, 512 / CTA)
   extern __shared__ double2 fsm[];
   uint32_t s, tid;
   if (p.rows) { s = threadIdx.x / T; tid = threadIdx.x % T; }
-  else { s = threadIdx.x % p.S; tid = threadIdx.x / p.S; }
+  else { s = threadIdx.x & (p.S - 1); tid = threadIdx.x >> p.logS; }
   const uint64_t seq0 = (uint64_t)blockIdx.x * p.S, seq = seq0 + s;
   const bool active = s < p.S && tid < (uint32_t)T;  // (a CTA narrower than 256 threads leaves some idle)
   const bool valid = active && seq < p.nseq;
@@ -278,22 +327,76 @@ __global__ void __launch_bounds__(CTA, 512 / CTA)
   __syncthreads();  // twiddle tables (and the staged bytes) visible to the CTA
   double2 a[16];
   FlatAcc fa;
-  fft_passes<LOGN, 0, IN, OUT>(p, io, a, Xs, tid, seq, active, valid, fa);
-  if (OUT == FFT_OUT_SPECTRUM && p.part) {  // fused flatness partials: fixed order -> deterministic
-    __shared__ double2 red[CTA / 32];
-    double2 acc = make_double2(fa.sum_log(), fa.sp);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1)
-      acc = make_double2(__dadd_rn(acc.x, __shfl_xor_sync(0xffffffffu, acc.x, o)),
-                         __dadd_rn(acc.y, __shfl_xor_sync(0xffffffffu, acc.y, o)));
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double2 t = red[0];
-      for (int w = 1; w < CTA / 32; ++w) t = make_double2(__dadd_rn(t.x, red[w].x), __dadd_rn(t.y, red[w].y));
-      p.part[blockIdx.x] = t;
+  fft_passes<LOGN, 0, IN, OUT>(p, io, a, Xs, tid, seq, active, valid, fa, no_prefetch);
+  if (OUT == FFT_OUT_SPECTRUM && p.part) flat_partial<CTA>(fa, p.part);
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+// issue the asynchronous copy of tile `tile` (S sequences of the batch) into shared memory:
+// complex input -> the padded exchange tile, bytes -> the 16-byte-per-thread stage
+template <int IN, int N, int LOGN, int CTA>
+__device__ __forceinline__ void fft_prefetch(const FftPass& p, const uint8_t* bytes, const double2* cin,
+                                             double2* fsm, uint4* stage, uint64_t tile) {
+  const uint64_t seq0 = tile * p.S;
+  const uint32_t nS = (uint32_t)((p.nseq - seq0 < p.S) ? p.nseq - seq0 : p.S);
+  if (IN == FFT_IN_COMPLEX) {
+    for (uint32_t e = threadIdx.x; e < (p.S << LOGN); e += CTA) {
+      const uint32_t s = p.rows ? e / N : e & (p.S - 1), idx = p.rows ? e % N : e >> p.logS;
+      if (s >= nS) continue;
+      const uint64_t g = p.rows ? (seq0 + s) * p.in_pitch + idx : (uint64_t)idx * p.in_pitch + seq0 + s;
+      cp_async16(fsm + (size_t)s * p.pitch + fft_pad(idx), cin + g);
     }
+  } else if ((uint64_t)threadIdx.x * 16 < (uint64_t)nS * N) {  // rows, pitch N, 16-byte aligned
+    cp_async16(stage + threadIdx.x, bytes + seq0 * N + 16 * (uint64_t)threadIdx.x);
   }
+  cp_async_commit();
+}
+
+// Persistent variant for n >= 1024: each CTA loops over tiles (grid = resident CTAs) and
+// prefetches tile i+1 with cp.async while tile i's last pass computes and stores, so loads
+// overlap compute even at one 512-thread CTA per SM. The first pass reads the prefetched tile.
+template <int IN, int OUT, int LOGN, int CTA>
+__global__ void __launch_bounds__(CTA, 512 / CTA)
+    fft_persistent_kernel(const FftPass p, const uint8_t* __restrict__ bytes, const double2* cin, double2* cout,
+                          double* __restrict__ rout, const unsigned long long* __restrict__ sum,
+                          double* __restrict__ lag0) {
+  constexpr int N = 1 << LOGN, T = N / 16;
+  static_assert(N >= 256, "persistent FFT needs >= 2 passes");
+  extern __shared__ double2 fsm[];
+  __shared__ uint4 stage[CTA];
+  __shared__ double2 tws[64 + N / 64];
+  uint32_t s, tid;
+  if (p.rows) { s = threadIdx.x / T; tid = threadIdx.x % T; }
+  else { s = threadIdx.x & (p.S - 1); tid = threadIdx.x >> p.logS; }
+  const bool active = s < p.S && tid < (uint32_t)T;
+  double2* Xs = fsm + (size_t)(active ? s : 0) * p.pitch;
+  const uint64_t tiles = (p.nseq + p.S - 1) / p.S;
+  uint64_t tile = blockIdx.x;
+  if (tile < tiles) fft_prefetch<IN, N, LOGN, CTA>(p, bytes, cin, fsm, stage, tile);
+  for (uint32_t i = threadIdx.x; i < 64 + N / 64; i += CTA) tws[i] = __ldg(p.tw + (i < 64 ? i : 64 * (i - 64)));
+  FftIo io{bytes, reinterpret_cast<const uint8_t*>(stage), 0, cin, cout, rout, lag0, 0.0, tws, tws + 64};
+  if (IN == FFT_IN_CENTRED) io.mean = __ddiv_rn((double)*sum, (double)p.H * (double)p.W);
+  double2 a[16];
+  FlatAcc fa;
+  for (; tile < tiles; tile += gridDim.x) {
+    cp_async_wait_all();
+    __syncthreads();  // the tile (and the twiddles) visible to the CTA
+    io.seq0 = tile * p.S;
+    const uint64_t seq = io.seq0 + s;
+    const bool valid = active && seq < p.nseq;
+    const uint64_t next = tile + gridDim.x;
+    auto pre = [&]() {
+      if (next < tiles) fft_prefetch<IN, N, LOGN, CTA>(p, bytes, cin, fsm, stage, next);
+    };
+    fft_passes<LOGN, 0, IN, OUT, true>(p, io, a, Xs, tid, seq, active, valid, fa, pre);
+  }
+  if (OUT == FFT_OUT_SPECTRUM && p.part) flat_partial<CTA>(fa, p.part);
 }
 
 // twiddle table exp(-2 pi i m / n), m < n
