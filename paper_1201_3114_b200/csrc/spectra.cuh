@@ -76,9 +76,10 @@ inline size_t fft_smem_bytes(const FftPass& p) {
 
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(__dadd_rn(a.x, b.x), __dadd_rn(a.y, b.y)); }
 __device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(__dsub_rn(a.x, b.x), __dsub_rn(a.y, b.y)); }
+// complex product with fused multiply-adds (4 FP64 pipe ops instead of 6; the FFTs are
+// analysis arithmetic with a tolerance, not part of the bit-exact cipher)
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
-  return make_double2(__dsub_rn(__dmul_rn(a.x, b.x), __dmul_rn(a.y, b.y)),
-                      __dadd_rn(__dmul_rn(a.x, b.y), __dmul_rn(a.y, b.x)));
+  return make_double2(__fma_rn(a.x, b.x, -__dmul_rn(a.y, b.y)), __fma_rn(a.x, b.y, __dmul_rn(a.y, b.x)));
 }
 
 // x * exp(-2 pi i m / 16), m a compile-time constant after unrolling: 1 and -i are free
@@ -414,8 +415,15 @@ constexpr int kFftCta = 256;  // the reductions below
 __global__ void __launch_bounds__(kFftCta) byte_sum_kernel(const uint8_t* __restrict__ x, uint64_t n,
                                                            unsigned long long* __restrict__ out) {
   unsigned long long acc = 0;
-  for (uint64_t i = (uint64_t)blockIdx.x * kFftCta + threadIdx.x; i < n; i += (uint64_t)gridDim.x * kFftCta)
-    acc += x[i];
+  const uint64_t t0 = (uint64_t)blockIdx.x * kFftCta + threadIdx.x, step = (uint64_t)gridDim.x * kFftCta;
+  if ((reinterpret_cast<uintptr_t>(x) & 15) == 0 && n % 16 == 0) {  // 16 bytes per load, SAD-summed
+    for (uint64_t i = t0; i < n / 16; i += step) {
+      const uint4 v = __ldcs(reinterpret_cast<const uint4*>(x) + i);
+      acc += __vsadu4(v.x, 0u) + __vsadu4(v.y, 0u) + __vsadu4(v.z, 0u) + __vsadu4(v.w, 0u);
+    }
+  } else {
+    for (uint64_t i = t0; i < n; i += step) acc += x[i];
+  }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
   if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, acc);
@@ -425,8 +433,16 @@ __global__ void __launch_bounds__(kFftCta) byte_sum_kernel(const uint8_t* __rest
 __global__ void __launch_bounds__(kFftCta) autocorr_normalise_kernel(double* __restrict__ r, uint64_t n,
                                                                      const double* __restrict__ lag0) {
   const double c0 = *lag0;
-  for (uint64_t i = (uint64_t)blockIdx.x * kFftCta + threadIdx.x; i < n; i += (uint64_t)gridDim.x * kFftCta)
-    r[i] = c0 == 0.0 ? (i == 0 ? 1.0 : 0.0) : __ddiv_rn(r[i], c0);
+  const uint64_t t0 = (uint64_t)blockIdx.x * kFftCta + threadIdx.x, step = (uint64_t)gridDim.x * kFftCta;
+  if (c0 != 0.0 && (reinterpret_cast<uintptr_t>(r) & 15) == 0 && n % 2 == 0) {  // 16-byte accesses
+    double2* r2 = reinterpret_cast<double2*>(r);
+    for (uint64_t i = t0; i < n / 2; i += step) {
+      const double2 v = r2[i];
+      r2[i] = make_double2(__ddiv_rn(v.x, c0), __ddiv_rn(v.y, c0));
+    }
+  } else {
+    for (uint64_t i = t0; i < n; i += step) r[i] = c0 == 0.0 ? (i == 0 ? 1.0 : 0.0) : __ddiv_rn(r[i], c0);
+  }
 }
 
 // spectral flatness = exp(mean log P) / mean P over the non-DC bins, from the per-CTA partials
