@@ -70,3 +70,34 @@ def test_message_beyond_4gib():
     ct[bad_b * (B + 16) + 100] ^= 0x20
     st, fb, _ = L.lorenz_verify(key, n, 0, nb, ct)
     assert st == L.E_INTEGRITY and fb == bad_b
+
+
+def test_host_api_bounded_device_memory():
+    """lorenz_encrypt_host / lorenz_decrypt_host on a 6 GiB + ragged HOST message: host offsets
+    past 2^32, and the device footprint stays at the 8-slot chunk ring (~2 GB), not the slice size
+    (the ring is what lets messages larger than HBM stream through)."""
+    n = (3 << 31) + 77  # 6 GiB + 77 bytes
+    pw = inputs.password(seed=45)
+    key = L.lorenz_keysetup(pw, mode=L.FAST, n_it=2)
+    nb = key.num_blocks(n)
+    rng = np.random.default_rng(7)
+    pt = rng.integers(0, 256, n, dtype=np.uint8)
+    ct = np.empty(key.ct_len(n), dtype=np.uint8)
+    torch.cuda.synchronize()
+    free0, _ = torch.cuda.mem_get_info()
+    tag = L.lorenz_encrypt_host(key, n, 0, nb, pt, ct)
+    free1, _ = torch.cuda.mem_get_info()
+    assert free0 - free1 < (3 << 30), f"device footprint {(free0 - free1) / 2**30:.2f} GiB"  # pool keeps the ring cached
+    prm = oracle.params(mode=oracle.FAST, n_it=2, block_size=B)
+    b32 = (1 << 32) // (B + 16)
+    for b in (0, b32 - 1, b32, b32 + 1, (1 << 32) // B, nb - 1):
+        lo = b * B
+        blk = pt[lo:min(n, lo + B)]
+        want = oracle.encrypt_block(pw, n, b, blk, prm)
+        assert np.array_equal(ct[b * (B + 16):b * (B + 16) + len(blk) + 16], want), f"block {b}"
+    tags = ct[:(nb - 1) * (B + 16)].reshape(nb - 1, B + 16)[:, B:]
+    want_tag = np.bitwise_xor.reduce(tags, axis=0) ^ ct[-16:]
+    assert tag == want_tag.tobytes()
+    back = np.empty(n, dtype=np.uint8)
+    st, fb = L.lorenz_decrypt_host(key, n, 0, nb, ct, back)
+    assert st == L.OK and fb == -1 and np.array_equal(back, pt)
