@@ -592,10 +592,11 @@ lz::FftPass fft_cols(uint32_t H, uint32_t W, const double2* tw, uint64_t in_pitc
 template <int IN, int OUT>
 bool fft_launch(const lz::FftPass& p, const uint8_t* bytes, const double2* cin, double2* cout, double* rout,
                 const unsigned long long* sum, double* lag0, cudaStream_t st, unsigned* grid_out = nullptr) {
-  const size_t smem = lz::fft_smem_bytes(p);
+  const size_t smem = lz::fft_smem_bytes(p, OUT == lz::FFT_OUT_R2C || OUT == lz::FFT_OUT_HALF_SPECTRUM);
   const unsigned tiles = (p.nseq + p.S - 1) / p.S, cta = lz::fft_cta(p.n, p.rows != 0);
   const bool persist =
-      p.logn >= 10 && (IN == lz::FFT_IN_COMPLEX || (p.rows && p.in_pitch == p.n && aligned16(bytes)));
+      p.logn >= 10 && OUT != lz::FFT_OUT_R2C && OUT != lz::FFT_OUT_HALF_SPECTRUM && IN != lz::FFT_IN_PAIRS &&
+      (IN == lz::FFT_IN_COMPLEX || (p.rows && p.in_pitch == p.n && aligned16(bytes)));
   auto go = [&](auto kernel) {
     if (!cuda_ok(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "fft smem"))
       return false;
@@ -632,6 +633,11 @@ bool fft_launch(const lz::FftPass& p, const uint8_t* bytes, const double2* cin, 
 }
 
 // twiddle tables for the row (W) and column (H) lengths: tw[0..W) then tw[W..W+H)
+bool fft_twiddle(double2* tw, uint32_t n, cudaStream_t st) {
+  lz::twiddle_kernel<<<(n + 255) / 256, 256, 0, st>>>(tw, n);
+  return cuda_ok(cudaGetLastError(), "twiddles");
+}
+
 bool fft_twiddles(double2* tw, uint32_t H, uint32_t W, cudaStream_t st) {
   lz::twiddle_kernel<<<(W + 255) / 256, 256, 0, st>>>(tw, W);
   lz::twiddle_kernel<<<(H + 255) / 256, 256, 0, st>>>(tw + W, H);
@@ -658,21 +664,39 @@ lorenz_status lorenz_power_spectrum(const uint8_t* x, uint32_t H, uint32_t W, do
   const uint64_t N = (uint64_t)H * W;
   double2* ws = nullptr;
   double2* part = nullptr;
-  const uint64_t Pw = fft_ws_pitch(W), NW = (uint64_t)H * Pw;
-  if (!cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&ws), (NW + H + W) * sizeof(double2), st), "alloc fft"))
+  // real input: W-point row transforms as W/2-point complex FFTs of byte pairs (FFT_IN_PAIRS ->
+  // FFT_OUT_R2C), then W/2 packed columns whose powers are written at (k, l) and (-k, -l)
+  // (FFT_OUT_HALF_SPECTRUM): half the FFT work and the workspace of the complex path. W = 2 keeps
+  // the complex path.
+  const bool r2c = W >= 4;
+  const uint32_t M = r2c ? W / 2 : W;
+  const uint64_t NW = (uint64_t)H * M;
+  if (!cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&ws), (NW + M + W + H) * sizeof(double2), st),
+               "alloc fft"))
     return LORENZ_E_CUDA;
-  double2* tw = ws + NW;
-  lz::FftPass rows = fft_rows(H, W, tw, W, Pw), cols = fft_cols(H, W, tw + W, Pw, W);
+  double2* tw_r = ws + NW;   // M-point (row FFTs)
+  double2* tw_2 = tw_r + M;  // W-point (R2C unpack)
+  double2* tw_c = tw_2 + W;  // H-point (column FFTs)
+  lz::FftPass rows = fft_rows(H, M, tw_r, W, M), cols = fft_cols(H, M, tw_c, M, W);
+  rows.W = cols.W = W;
+  rows.tw2 = tw_2;
   cols.scale = std::ldexp(1.0, -2 * (int)ilog2((uint32_t)N));  // 1 / N^2
   const uint32_t tiles = (cols.nseq + cols.S - 1) / cols.S;  // >= the column pass's grid
   unsigned nparts = 0;                                          // one flatness partial per column CTA
   bool ok = !flatness ||
             cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&part), tiles * sizeof(double2), st), "alloc");
   cols.part = flatness ? part : nullptr;
-  ok = ok && fft_twiddles(tw, H, W, st) &&
-       fft_launch<lz::FFT_IN_BYTES, lz::FFT_OUT_COMPLEX>(rows, x, nullptr, ws, nullptr, nullptr, nullptr, st) &&
-       fft_launch<lz::FFT_IN_COMPLEX, lz::FFT_OUT_SPECTRUM>(cols, nullptr, ws, ws, power, nullptr, nullptr, st,
-                                                            &nparts);
+  ok = ok && fft_twiddle(tw_r, M, st) && fft_twiddle(tw_2, W, st) && fft_twiddle(tw_c, H, st);
+  if (r2c)
+    ok = ok &&
+         fft_launch<lz::FFT_IN_PAIRS, lz::FFT_OUT_R2C>(rows, x, nullptr, ws, nullptr, nullptr, nullptr, st) &&
+         fft_launch<lz::FFT_IN_COMPLEX, lz::FFT_OUT_HALF_SPECTRUM>(cols, nullptr, ws, ws, power, nullptr, nullptr,
+                                                                   st, &nparts);
+  else
+    ok = ok &&
+         fft_launch<lz::FFT_IN_BYTES, lz::FFT_OUT_COMPLEX>(rows, x, nullptr, ws, nullptr, nullptr, nullptr, st) &&
+         fft_launch<lz::FFT_IN_COMPLEX, lz::FFT_OUT_SPECTRUM>(cols, nullptr, ws, ws, power, nullptr, nullptr, st,
+                                                              &nparts);
   if (ok && flatness) {
     lz::flatness_final_kernel<<<1, lz::kFftCta, 0, st>>>(part, nparts, N - 1, flatness);
     ok = cuda_ok(cudaGetLastError(), "flatness");

@@ -24,8 +24,16 @@ namespace lz {
 
 constexpr int kFftCtaThreads = 256;
 
-enum FftIn : int { FFT_IN_BYTES = 0, FFT_IN_CENTRED = 1, FFT_IN_COMPLEX = 2 };
-enum FftOut : int { FFT_OUT_COMPLEX = 0, FFT_OUT_POWER = 1, FFT_OUT_SPECTRUM = 2, FFT_OUT_REAL = 3 };
+// FFT_IN_PAIRS: a real row of 2n bytes read as n complex values x[2m] + i x[2m+1] (real-to-complex)
+enum FftIn : int { FFT_IN_BYTES = 0, FFT_IN_CENTRED = 1, FFT_IN_COMPLEX = 2, FFT_IN_PAIRS = 3 };
+// FFT_OUT_R2C: unpack the row's half spectrum X[0..n] (2n-point real DFT) from the n-point complex
+//   FFT of the pairs, stored as n complex values with X[0] + i X[n] packed in element 0.
+// FFT_OUT_HALF_SPECTRUM: column pass over those n packed columns: |F|^2 / N^2 at (k, l) and at its
+//   mirror (-k, W-l) (real input: P(k,l) = P(-k,-l)); column 0 unpacks the DC and Nyquist columns.
+enum FftOut : int {
+  FFT_OUT_COMPLEX = 0, FFT_OUT_POWER = 1, FFT_OUT_SPECTRUM = 2, FFT_OUT_REAL = 3,
+  FFT_OUT_R2C = 4, FFT_OUT_HALF_SPECTRUM = 5
+};
 
 struct FftPass {
   uint32_t n, logn;     // FFT length (power of two, 2..4096) and log2(n)
@@ -41,6 +49,7 @@ struct FftPass {
   uint32_t H, W;        // matrix shape (for the DC shift)
   double scale;         // FFT_OUT_SPECTRUM: 1 / (HW)^2 (a power of two: exact)
   const double2* tw;    // exp(-2 pi i m / n), m < n
+  const double2* tw2;   // FFT_OUT_R2C: exp(-2 pi i m / 2n), m < 2n
   double2* part;        // FFT_OUT_SPECTRUM (nullable): per-CTA (sum log P, sum P) over non-DC bins
 };
 
@@ -70,8 +79,9 @@ inline FftPass fft_plan(uint32_t n, uint32_t logn, uint32_t nseq, bool rows) {
   if (L) p.rlog[p.npass++] = L;
   return p;
 }
-inline size_t fft_smem_bytes(const FftPass& p) {
-  return p.npass > 1 ? (size_t)p.S * p.pitch * 16 : 0;
+// exchange tile (>= 2 passes) or shared-memory epilogue (R2C / half-spectrum modes)
+inline size_t fft_smem_bytes(const FftPass& p, bool epilogue = false) {
+  return (p.npass > 1 || epilogue) ? (size_t)p.S * p.pitch * 16 : 0;
 }
 
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(__dadd_rn(a.x, b.x), __dadd_rn(a.y, b.y)); }
@@ -173,6 +183,10 @@ __device__ __forceinline__ double2 twid(const FftIo& io, uint32_t m) {
 
 template <int IN, int N>
 __device__ __forceinline__ double2 fft_load(const FftPass& p, const FftIo& io, uint64_t seq, uint32_t idx) {
+  if (IN == FFT_IN_PAIRS) {  // rows only: bytes 2 idx, 2 idx + 1 of row seq
+    const uint8_t* r = io.sb ? io.sb + (seq - io.seq0) * 2 * N : io.bytes + seq * p.in_pitch;
+    return make_double2((double)r[2 * idx], (double)r[2 * idx + 1]);
+  }
   const uint64_t g = p.rows ? seq * p.in_pitch + idx : (uint64_t)idx * p.in_pitch + seq;
   if (IN == FFT_IN_COMPLEX) return io.cin[g];
   const double b = io.sb ? (double)io.sb[(seq - io.seq0) * N + idx] : (double)io.bytes[g];
@@ -192,6 +206,12 @@ __device__ __forceinline__ void fft_store(const FftPass& p, const FftIo& io, uin
     const double P = __dmul_rn(__dadd_rn(__dmul_rn(v.x, v.x), __dmul_rn(v.y, v.y)), p.scale);
     io.rout[o] = P;
     if (p.part && (i | j) != 0) acc.add(P);  // flatness over the non-DC bins
+  } else if (OUT == FFT_OUT_HALF_SPECTRUM) {  // column j in [1, W/2): (k, j) and its mirror (-k, W - j)
+    const double P = __dmul_rn(__dadd_rn(__dmul_rn(v.x, v.x), __dmul_rn(v.y, v.y)), p.scale);
+    const uint64_t i2 = (p.H - i) & (p.H - 1), j2 = p.W - j;
+    io.rout[((i + p.H / 2) & (p.H - 1)) * p.W + ((j + p.W / 2) & (p.W - 1))] = P;
+    io.rout[((i2 + p.H / 2) & (p.H - 1)) * p.W + ((j2 + p.W / 2) & (p.W - 1))] = P;
+    if (p.part) { acc.add(P); acc.add(P); }
   } else {
     io.rout[i * p.W + j] = v.x;
     if ((i | j) == 0) *io.lag0 = v.x;
@@ -250,14 +270,14 @@ __device__ __forceinline__ void fft_pass(const FftPass& p, const FftIo& io, doub
     for (int u = 0; u < R; ++u) {
       const uint32_t pos = (j - k) * R + k + u * LS;
       const double2 v = a[g * R + bitrev_c<R>(u)];
-      if (LAST) {
+      if (LAST && !(OUT == FFT_OUT_R2C || (OUT == FFT_OUT_HALF_SPECTRUM && seq == 0))) {
         if (valid) fft_store<OUT>(p, io, seq, pos, v, acc);
       } else {
-        Xs[fft_pad(pos)] = v;
+        Xs[fft_pad(pos)] = v;  // exchange, or the input of a shared-memory epilogue
       }
     }
   }
-  if (!LAST) __syncthreads();
+  if (!LAST || OUT == FFT_OUT_R2C || OUT == FFT_OUT_HALF_SPECTRUM) __syncthreads();
 }
 
 // the passes of an N = 2^LOGN transform: radix 16 while >= 4 bits remain, then the remainder
@@ -294,6 +314,54 @@ __device__ __forceinline__ void flat_partial(const FlatAcc& fa, double2* part) {
   }
 }
 
+// FFT_OUT_R2C epilogue: Z = the n-point FFT of z[m] = x[2m] + i x[2m+1] is in Xs (natural order).
+// With a = Z[l], b = conj(Z[n-l]): Fe = (a + b)/2, Fo = -i (a - b)/2, w = exp(-2 pi i l / 2n):
+// X[l] = Fe + w Fo and X[n-l] = conj(Fe - w Fo); X[0] = Re Z0 + Im Z0 and X[n] = Re Z0 - Im Z0 are
+// stored packed as X[0] + i X[n] in element 0.
+template <int N>
+__device__ __forceinline__ void r2c_epilogue(const FftPass& p, const FftIo& io, const double2* Xs, uint32_t tid,
+                                             uint64_t seq, bool valid, const double2* t2lo, const double2* t2hi) {
+  constexpr int T = N < 16 ? 1 : N / 16;
+  if (!valid) return;
+  double2* y = io.cout + seq * p.out_pitch;
+  for (uint32_t l = tid; l <= N / 2; l += T) {
+    const double2 a = Xs[fft_pad(l)], bz = Xs[fft_pad((N - l) & (N - 1))];
+    if (l == 0) {
+      y[0] = make_double2(__dadd_rn(a.x, a.y), __dsub_rn(a.x, a.y));
+      continue;
+    }
+    const double2 fe = make_double2(__dmul_rn(__dadd_rn(a.x, bz.x), 0.5), __dmul_rn(__dsub_rn(a.y, bz.y), 0.5));
+    const double2 fo = make_double2(__dmul_rn(__dadd_rn(a.y, bz.y), 0.5), __dmul_rn(__dsub_rn(bz.x, a.x), 0.5));
+    const double2 w = (2 * N <= 64) ? t2lo[l] : cmul(t2lo[l & 63], t2hi[l >> 6]);
+    const double2 wf = cmul(w, fo);
+    y[l] = make_double2(__dadd_rn(fe.x, wf.x), __dadd_rn(fe.y, wf.y));
+    if (l != N / 2) y[N - l] = make_double2(__dsub_rn(fe.x, wf.x), __dsub_rn(wf.y, fe.y));
+  }
+}
+
+// FFT_OUT_HALF_SPECTRUM epilogue for column 0 (sequence 0): U = FFT(X[.,0] + i X[.,W/2]) is in Xs.
+// A[k] = (U[k] + conj(U[-k]))/2 and B[k] = -i (U[k] - conj(U[-k]))/2 are the spectra of the DC and
+// Nyquist columns: P(k, 0) = |A|^2 / N^2, P(k, W/2) = |B|^2 / N^2.
+template <int N>
+__device__ __forceinline__ void half_col0_epilogue(const FftPass& p, const FftIo& io, const double2* Xs,
+                                                   uint32_t tid, FlatAcc& acc) {
+  constexpr int T = N < 16 ? 1 : N / 16;
+  for (uint32_t k = tid; k < N; k += T) {
+    const double2 a = Xs[fft_pad(k)], bz = Xs[fft_pad((N - k) & (N - 1))];
+    const double2 A = make_double2(__dmul_rn(__dadd_rn(a.x, bz.x), 0.5), __dmul_rn(__dsub_rn(a.y, bz.y), 0.5));
+    const double2 Bv = make_double2(__dmul_rn(__dadd_rn(a.y, bz.y), 0.5), __dmul_rn(__dsub_rn(bz.x, a.x), 0.5));
+    const double P0 = __dmul_rn(__dadd_rn(__dmul_rn(A.x, A.x), __dmul_rn(A.y, A.y)), p.scale);
+    const double P1 = __dmul_rn(__dadd_rn(__dmul_rn(Bv.x, Bv.x), __dmul_rn(Bv.y, Bv.y)), p.scale);
+    const uint64_t row = ((k + p.H / 2) & (p.H - 1)) * p.W;
+    io.rout[row + p.W / 2] = P0;  // column 0 -> centred column W/2
+    io.rout[row] = P1;            // column W/2 -> centred column 0
+    if (p.part) {
+      if (k != 0) acc.add(P0);
+      acc.add(P1);
+    }
+  }
+}
+
 // CTA = S sequences x T = N/16 threads (T = 1 when N < 16); rows: a sequence's threads are
 // adjacent; columns: adjacent threads take adjacent columns (coalescing). Byte-input row passes
 // first stage the CTA's rows (S N = 4096 bytes) in shared memory with one 16-byte load per thread.
@@ -317,19 +385,32 @@ __global__ void __launch_bounds__(CTA, 512 / CTA)
   FftIo io{bytes, nullptr, seq0, cin, cout, rout, lag0, 0.0, tws, tws + 64};
   if (IN == FFT_IN_CENTRED) io.mean = __ddiv_rn((double)*sum, (double)p.H * (double)p.W);
   if constexpr (IN != FFT_IN_COMPLEX && N >= 16 && CTA == 256) {
-    __shared__ uint4 stage[CTA];  // S N = CTA * 16 bytes
-    if (p.rows && p.in_pitch == N && (reinterpret_cast<uintptr_t>(bytes) & 15) == 0) {
+    constexpr int BPE = IN == FFT_IN_PAIRS ? 2 : 1;  // bytes per element
+    __shared__ uint4 stage[CTA * BPE];                // S N BPE = CTA * 16 * BPE bytes
+    if (p.rows && p.in_pitch == (uint64_t)N * BPE && (reinterpret_cast<uintptr_t>(bytes) & 15) == 0) {
       const uint64_t rows = (p.nseq - seq0 < p.S) ? p.nseq - seq0 : p.S;
-      if ((uint64_t)threadIdx.x * 16 < rows * N)
-        stage[threadIdx.x] = __ldg(reinterpret_cast<const uint4*>(bytes + seq0 * N) + threadIdx.x);
+      const uint4* src = reinterpret_cast<const uint4*>(bytes + seq0 * N * BPE);
+#pragma unroll
+      for (int q = 0; q < BPE; ++q) {
+        const uint32_t i = threadIdx.x + q * CTA;
+        if ((uint64_t)i * 16 < rows * N * BPE) stage[i] = __ldg(src + i);
+      }
       io.sb = reinterpret_cast<const uint8_t*>(stage);
     }
   }
+  __shared__ double2 tw2s[OUT == FFT_OUT_R2C ? 64 + (2 * N > 64 ? 2 * N / 64 : 1) : 1];
+  if (OUT == FFT_OUT_R2C)
+    for (uint32_t i = threadIdx.x; i < 64 + (2 * N > 64 ? 2 * N / 64 : 0); i += CTA)
+      if (i < 64) { if (i < 2u * N) tw2s[i] = __ldg(p.tw2 + i); }
+      else tw2s[i] = __ldg(p.tw2 + 64 * (i - 64));
   __syncthreads();  // twiddle tables (and the staged bytes) visible to the CTA
   double2 a[16];
   FlatAcc fa;
   fft_passes<LOGN, 0, IN, OUT>(p, io, a, Xs, tid, seq, active, valid, fa, no_prefetch);
-  if (OUT == FFT_OUT_SPECTRUM && p.part) flat_partial<CTA>(fa, p.part);
+  if constexpr (OUT == FFT_OUT_R2C) r2c_epilogue<N>(p, io, Xs, tid, seq, valid, tw2s, tw2s + 64);
+  if constexpr (OUT == FFT_OUT_HALF_SPECTRUM)
+    if (seq0 == 0 && s == 0 && active) half_col0_epilogue<N>(p, io, Xs, tid, fa);
+  if ((OUT == FFT_OUT_SPECTRUM || OUT == FFT_OUT_HALF_SPECTRUM) && p.part) flat_partial<CTA>(fa, p.part);
 }
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
