@@ -592,10 +592,11 @@ lz::FftPass fft_cols(uint32_t H, uint32_t W, const double2* tw, uint64_t in_pitc
 template <int IN, int OUT>
 bool fft_launch(const lz::FftPass& p, const uint8_t* bytes, const double2* cin, double2* cout, double* rout,
                 const unsigned long long* sum, double* lag0, cudaStream_t st, unsigned* grid_out = nullptr) {
-  const size_t smem = lz::fft_smem_bytes(p, OUT == lz::FFT_OUT_R2C || OUT == lz::FFT_OUT_HALF_SPECTRUM);
+  const size_t smem = lz::fft_smem_bytes(
+      p, OUT == lz::FFT_OUT_R2C || OUT == lz::FFT_OUT_HALF_SPECTRUM || OUT == lz::FFT_OUT_POWER_FFT);
   const unsigned tiles = (p.nseq + p.S - 1) / p.S, cta = lz::fft_cta(p.n, p.rows != 0);
   const bool persist =
-      p.logn >= 10 && OUT != lz::FFT_OUT_R2C && OUT != lz::FFT_OUT_HALF_SPECTRUM && IN != lz::FFT_IN_PAIRS &&
+      p.logn >= 10 && OUT <= lz::FFT_OUT_REAL && IN <= lz::FFT_IN_COMPLEX &&  // plain modes only
       (IN == lz::FFT_IN_COMPLEX || (p.rows && p.in_pitch == p.n && aligned16(bytes)));
   auto go = [&](auto kernel) {
     if (!cuda_ok(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "fft smem"))
@@ -638,11 +639,6 @@ bool fft_twiddle(double2* tw, uint32_t n, cudaStream_t st) {
   return cuda_ok(cudaGetLastError(), "twiddles");
 }
 
-bool fft_twiddles(double2* tw, uint32_t H, uint32_t W, cudaStream_t st) {
-  lz::twiddle_kernel<<<(W + 255) / 256, 256, 0, st>>>(tw, W);
-  lz::twiddle_kernel<<<(H + 255) / 256, 256, 0, st>>>(tw + W, H);
-  return cuda_ok(cudaGetLastError(), "twiddles");
-}
 
 lorenz_status spectra_args(const uint8_t* x, uint32_t H, uint32_t W, const double* out) {
   if (!x || !out || !fft_side(H) || !fft_side(W) || (reinterpret_cast<uintptr_t>(out) & 7)) {
@@ -715,22 +711,43 @@ lorenz_status lorenz_autocorrelation(const uint8_t* x, uint32_t H, uint32_t W, d
   const uint64_t N = (uint64_t)H * W;
   double2* ws = nullptr;
   unsigned long long* aux = nullptr;  // [0] = byte sum, [1] = lag-0 value (double bits)
-  const uint64_t Pw = fft_ws_pitch(W), NW = (uint64_t)H * Pw;
-  if (!cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&ws), (NW + H + W) * sizeof(double2), st), "alloc fft") ||
+  // real input (W >= 4): R2C rows of centred byte pairs -> one fused column pass (transform, |.|^2,
+  // transform: FFT_OUT_POWER_FFT) over the W/2 packed columns -> C2R rows -> normalisation.
+  // Three transform passes over a half-size workspace instead of four full ones; W = 2 keeps the
+  // complex path.
+  const bool r2c = W >= 4;
+  const uint32_t M = r2c ? W / 2 : W;
+  const uint64_t Pw = r2c ? M : fft_ws_pitch(W), NW = (uint64_t)H * Pw;
+  if (!cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&ws), (NW + M + W + H) * sizeof(double2), st),
+               "alloc fft") ||
       !cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&aux), 16, st), "alloc aux")) {
     if (ws) cudaFreeAsync(ws, st);
     return LORENZ_E_CUDA;
   }
   double* lag0 = reinterpret_cast<double*>(aux + 1);
-  double2* tw = ws + NW;
-  const lz::FftPass rows1 = fft_rows(H, W, tw, W, Pw), cols1 = fft_cols(H, W, tw + W, Pw, Pw);
-  const lz::FftPass rows2 = fft_rows(H, W, tw, Pw, Pw), cols2 = fft_cols(H, W, tw + W, Pw, W);
+  double2* tw_r = ws + NW;   // M-point (row FFTs)
+  double2* tw_2 = tw_r + M;  // W-point (R2C / C2R)
+  double2* tw_c = tw_2 + W;  // H-point (column FFTs)
   const unsigned sgrid = (unsigned)std::min<uint64_t>(4ull * sm_count(), (N + lz::kFftCta - 1) / lz::kFftCta);
-  bool ok = cuda_ok(cudaMemsetAsync(aux, 0, 16, st), "memset") && fft_twiddles(tw, H, W, st);
+  bool ok = cuda_ok(cudaMemsetAsync(aux, 0, 16, st), "memset") && fft_twiddle(tw_r, M, st) &&
+            fft_twiddle(tw_2, W, st) && fft_twiddle(tw_c, H, st);
   if (ok) {
     lz::byte_sum_kernel<<<sgrid, lz::kFftCta, 0, st>>>(x, N, aux);
-    ok = cuda_ok(cudaGetLastError(), "byte sum") &&
-         fft_launch<lz::FFT_IN_CENTRED, lz::FFT_OUT_COMPLEX>(rows1, x, nullptr, ws, nullptr, aux, nullptr, st) &&
+    ok = cuda_ok(cudaGetLastError(), "byte sum");
+  }
+  if (ok && r2c) {
+    lz::FftPass rows1 = fft_rows(H, M, tw_r, W, M), cols = fft_cols(H, M, tw_c, M, M);
+    lz::FftPass rows2 = fft_rows(H, M, tw_r, M, M);
+    rows1.W = cols.W = rows2.W = W;
+    rows1.tw2 = rows2.tw2 = tw_2;
+    cols.packed0 = 1;
+    ok = fft_launch<lz::FFT_IN_PAIRS_CENTRED, lz::FFT_OUT_R2C>(rows1, x, nullptr, ws, nullptr, aux, nullptr, st) &&
+         fft_launch<lz::FFT_IN_COMPLEX, lz::FFT_OUT_POWER_FFT>(cols, nullptr, ws, ws, nullptr, nullptr, nullptr, st) &&
+         fft_launch<lz::FFT_IN_C2R, lz::FFT_OUT_REAL_PAIRS>(rows2, nullptr, ws, nullptr, r, nullptr, lag0, st);
+  } else if (ok) {
+    const lz::FftPass rows1 = fft_rows(H, W, tw_2, W, Pw), cols1 = fft_cols(H, W, tw_c, Pw, Pw);
+    const lz::FftPass rows2 = fft_rows(H, W, tw_2, Pw, Pw), cols2 = fft_cols(H, W, tw_c, Pw, W);
+    ok = fft_launch<lz::FFT_IN_CENTRED, lz::FFT_OUT_COMPLEX>(rows1, x, nullptr, ws, nullptr, aux, nullptr, st) &&
          fft_launch<lz::FFT_IN_COMPLEX, lz::FFT_OUT_POWER>(cols1, nullptr, ws, ws, nullptr, nullptr, nullptr, st) &&
          fft_launch<lz::FFT_IN_COMPLEX, lz::FFT_OUT_COMPLEX>(rows2, nullptr, ws, ws, nullptr, nullptr, nullptr, st) &&
          fft_launch<lz::FFT_IN_COMPLEX, lz::FFT_OUT_REAL>(cols2, nullptr, ws, nullptr, r, nullptr, lag0, st);

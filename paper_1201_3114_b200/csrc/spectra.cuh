@@ -25,14 +25,23 @@ namespace lz {
 constexpr int kFftCtaThreads = 256;
 
 // FFT_IN_PAIRS: a real row of 2n bytes read as n complex values x[2m] + i x[2m+1] (real-to-complex)
-enum FftIn : int { FFT_IN_BYTES = 0, FFT_IN_CENTRED = 1, FFT_IN_COMPLEX = 2, FFT_IN_PAIRS = 3 };
+// FFT_IN_PAIRS_CENTRED: the same with the mean subtracted (exact).
+// FFT_IN_C2R: a Hermitian half spectrum Q[0..n] (Q[0] + i Q[n] packed in element 0, both real)
+//   pre-processed so that one n-point FFT yields the real 2n-point transform (see c2r_load).
+enum FftIn : int {
+  FFT_IN_BYTES = 0, FFT_IN_CENTRED = 1, FFT_IN_COMPLEX = 2, FFT_IN_PAIRS = 3, FFT_IN_PAIRS_CENTRED = 4,
+  FFT_IN_C2R = 5
+};
 // FFT_OUT_R2C: unpack the row's half spectrum X[0..n] (2n-point real DFT) from the n-point complex
 //   FFT of the pairs, stored as n complex values with X[0] + i X[n] packed in element 0.
 // FFT_OUT_HALF_SPECTRUM: column pass over those n packed columns: |F|^2 / N^2 at (k, l) and at its
 //   mirror (-k, W-l) (real input: P(k,l) = P(-k,-l)); column 0 unpacks the DC and Nyquist columns.
+// FFT_OUT_POWER_FFT: column pass fusing transform -> |.|^2 (packed DC / Nyquist column unpacked) ->
+//   transform again (the autocorrelation's two column transforms in one HBM round trip).
+// FFT_OUT_REAL_PAIRS: the C2R row output R[m] -> real samples (2m, 2m+1) = (Re R, -Im R).
 enum FftOut : int {
   FFT_OUT_COMPLEX = 0, FFT_OUT_POWER = 1, FFT_OUT_SPECTRUM = 2, FFT_OUT_REAL = 3,
-  FFT_OUT_R2C = 4, FFT_OUT_HALF_SPECTRUM = 5
+  FFT_OUT_R2C = 4, FFT_OUT_HALF_SPECTRUM = 5, FFT_OUT_POWER_FFT = 6, FFT_OUT_REAL_PAIRS = 7
 };
 
 struct FftPass {
@@ -49,7 +58,8 @@ struct FftPass {
   uint32_t H, W;        // matrix shape (for the DC shift)
   double scale;         // FFT_OUT_SPECTRUM: 1 / (HW)^2 (a power of two: exact)
   const double2* tw;    // exp(-2 pi i m / n), m < n
-  const double2* tw2;   // FFT_OUT_R2C: exp(-2 pi i m / 2n), m < 2n
+  const double2* tw2;   // FFT_OUT_R2C / FFT_IN_C2R: exp(-2 pi i m / 2n), m < 2n
+  uint32_t packed0;     // FFT_OUT_POWER_FFT: sequence 0 holds the packed DC + i Nyquist column
   double2* part;        // FFT_OUT_SPECTRUM (nullable): per-CTA (sum log P, sum P) over non-DC bins
 };
 
@@ -172,7 +182,15 @@ struct FftIo {
   double mean;
   const double2* tlo;    // shared: exp(-2 pi i m / n), m < 64
   const double2* thi;    // shared: exp(-2 pi i 64 m / n), m < n / 64
+  const double2* t2lo;   // shared (R2C / C2R): exp(-2 pi i m / 2n), m < 64
+  const double2* t2hi;   // shared (R2C / C2R): exp(-2 pi i 64 m / 2n), m < 2n / 64
 };
+
+template <int N>
+__device__ __forceinline__ double2 twid2(const FftIo& io, uint32_t m) {  // exp(-2 pi i m / 2N)
+  if (2 * N <= 64) return io.t2lo[m];
+  return cmul(io.t2lo[m & 63], io.t2hi[m >> 6]);
+}
 
 // exp(-2 pi i m / n) = tlo[m mod 64] * thi[m / 64] (n <= 4096: two 64-entry shared tables)
 template <int N>
@@ -183,9 +201,22 @@ __device__ __forceinline__ double2 twid(const FftIo& io, uint32_t m) {
 
 template <int IN, int N>
 __device__ __forceinline__ double2 fft_load(const FftPass& p, const FftIo& io, uint64_t seq, uint32_t idx) {
-  if (IN == FFT_IN_PAIRS) {  // rows only: bytes 2 idx, 2 idx + 1 of row seq
+  if (IN == FFT_IN_PAIRS || IN == FFT_IN_PAIRS_CENTRED) {  // rows only: bytes 2 idx, 2 idx + 1 of row seq
     const uint8_t* r = io.sb ? io.sb + (seq - io.seq0) * 2 * N : io.bytes + seq * p.in_pitch;
-    return make_double2((double)r[2 * idx], (double)r[2 * idx + 1]);
+    if (IN == FFT_IN_PAIRS) return make_double2((double)r[2 * idx], (double)r[2 * idx + 1]);
+    return make_double2(__dsub_rn((double)r[2 * idx], io.mean), __dsub_rn((double)r[2 * idx + 1], io.mean));
+  }
+  if (IN == FFT_IN_C2R) {  // rows only: V[l] = Ge - i Go, Ge = (Q[l] + conj Q[n-l]) / 2, Go = w (Q[l] - conj Q[n-l]) / 2
+    const double2* q = io.cin + seq * p.in_pitch;
+    const double2 a = q[idx];
+    if (idx == 0) {  // Q[0], Q[n] real, packed in element 0
+      return make_double2(__dmul_rn(__dadd_rn(a.x, a.y), 0.5), __dmul_rn(__dsub_rn(a.y, a.x), 0.5));
+    }
+    const double2 b = q[N - idx];  // conj(b) = conj Q[n-l]
+    const double2 ge = make_double2(__dmul_rn(__dadd_rn(a.x, b.x), 0.5), __dmul_rn(__dsub_rn(a.y, b.y), 0.5));
+    const double2 d = make_double2(__dmul_rn(__dsub_rn(a.x, b.x), 0.5), __dmul_rn(__dadd_rn(a.y, b.y), 0.5));
+    const double2 go = cmul(twid2<N>(io, idx), d);
+    return make_double2(__dadd_rn(ge.x, go.y), __dsub_rn(ge.y, go.x));  // ge - i go
   }
   const uint64_t g = p.rows ? seq * p.in_pitch + idx : (uint64_t)idx * p.in_pitch + seq;
   if (IN == FFT_IN_COMPLEX) return io.cin[g];
@@ -206,6 +237,9 @@ __device__ __forceinline__ void fft_store(const FftPass& p, const FftIo& io, uin
     const double P = __dmul_rn(__dadd_rn(__dmul_rn(v.x, v.x), __dmul_rn(v.y, v.y)), p.scale);
     io.rout[o] = P;
     if (p.part && (i | j) != 0) acc.add(P);  // flatness over the non-DC bins
+  } else if (OUT == FFT_OUT_REAL_PAIRS) {  // rows only: samples (seq, 2 pos), (seq, 2 pos + 1)
+    reinterpret_cast<double2*>(io.rout + seq * p.W)[pos] = make_double2(v.x, -v.y);
+    if (seq == 0 && pos == 0) *io.lag0 = v.x;
   } else if (OUT == FFT_OUT_HALF_SPECTRUM) {  // column j in [1, W/2): (k, j) and its mirror (-k, W - j)
     const double P = __dmul_rn(__dadd_rn(__dmul_rn(v.x, v.x), __dmul_rn(v.y, v.y)), p.scale);
     const uint64_t i2 = (p.H - i) & (p.H - 1), j2 = p.W - j;
@@ -270,14 +304,14 @@ __device__ __forceinline__ void fft_pass(const FftPass& p, const FftIo& io, doub
     for (int u = 0; u < R; ++u) {
       const uint32_t pos = (j - k) * R + k + u * LS;
       const double2 v = a[g * R + bitrev_c<R>(u)];
-      if (LAST && !(OUT == FFT_OUT_R2C || (OUT == FFT_OUT_HALF_SPECTRUM && seq == 0))) {
+      if (LAST && !(OUT == FFT_OUT_R2C || OUT == FFT_OUT_POWER_FFT || (OUT == FFT_OUT_HALF_SPECTRUM && seq == 0))) {
         if (valid) fft_store<OUT>(p, io, seq, pos, v, acc);
       } else {
         Xs[fft_pad(pos)] = v;  // exchange, or the input of a shared-memory epilogue
       }
     }
   }
-  if (!LAST || OUT == FFT_OUT_R2C || OUT == FFT_OUT_HALF_SPECTRUM) __syncthreads();
+  if (!LAST || OUT == FFT_OUT_R2C || OUT == FFT_OUT_HALF_SPECTRUM || OUT == FFT_OUT_POWER_FFT) __syncthreads();
 }
 
 // the passes of an N = 2^LOGN transform: radix 16 while >= 4 bits remain, then the remainder
@@ -362,6 +396,32 @@ __device__ __forceinline__ void half_col0_epilogue(const FftPass& p, const FftIo
   }
 }
 
+// FFT_OUT_POWER_FFT middle step, in place in Xs: X -> |X|^2 (as (P, 0)); the packed column 0
+// (sequence 0 when p.packed0) -> (|A|^2, |B|^2) with A, B the DC / Nyquist column spectra
+// (A[k] = (U[k] + conj U[-k]) / 2, B[k] = -i (U[k] - conj U[-k]) / 2; both even in k).
+template <int N>
+__device__ __forceinline__ void power_in_place(const FftPass& p, double2* Xs, uint32_t tid, uint64_t seq,
+                                               bool active) {
+  constexpr int T = N < 16 ? 1 : N / 16;
+  if (!active) return;
+  for (uint32_t k = tid; k <= N / 2; k += T) {
+    const uint32_t k2 = (N - k) & (N - 1);
+    const double2 a = Xs[fft_pad(k)], bz = Xs[fft_pad(k2)];
+    double2 va, vb;
+    if (p.packed0 && seq == 0) {
+      const double2 A = make_double2(__dmul_rn(__dadd_rn(a.x, bz.x), 0.5), __dmul_rn(__dsub_rn(a.y, bz.y), 0.5));
+      const double2 Bv = make_double2(__dmul_rn(__dadd_rn(a.y, bz.y), 0.5), __dmul_rn(__dsub_rn(bz.x, a.x), 0.5));
+      va = vb = make_double2(__dadd_rn(__dmul_rn(A.x, A.x), __dmul_rn(A.y, A.y)),
+                             __dadd_rn(__dmul_rn(Bv.x, Bv.x), __dmul_rn(Bv.y, Bv.y)));
+    } else {
+      va = make_double2(__dadd_rn(__dmul_rn(a.x, a.x), __dmul_rn(a.y, a.y)), 0.0);
+      vb = make_double2(__dadd_rn(__dmul_rn(bz.x, bz.x), __dmul_rn(bz.y, bz.y)), 0.0);
+    }
+    Xs[fft_pad(k)] = va;
+    Xs[fft_pad(k2)] = vb;
+  }
+}
+
 // CTA = S sequences x T = N/16 threads (T = 1 when N < 16); rows: a sequence's threads are
 // adjacent; columns: adjacent threads take adjacent columns (coalescing). Byte-input row passes
 // first stage the CTA's rows (S N = 4096 bytes) in shared memory with one 16-byte load per thread.
@@ -382,10 +442,12 @@ __global__ void __launch_bounds__(CTA, 512 / CTA)
   for (uint32_t i = threadIdx.x; i < 64 + (N > 64 ? N / 64 : 0); i += CTA)
     if (i < 64) { if (i < (uint32_t)N) tws[i] = __ldg(p.tw + i); }
     else tws[i] = __ldg(p.tw + 64 * (i - 64));
-  FftIo io{bytes, nullptr, seq0, cin, cout, rout, lag0, 0.0, tws, tws + 64};
-  if (IN == FFT_IN_CENTRED) io.mean = __ddiv_rn((double)*sum, (double)p.H * (double)p.W);
-  if constexpr (IN != FFT_IN_COMPLEX && N >= 16 && CTA == 256) {
-    constexpr int BPE = IN == FFT_IN_PAIRS ? 2 : 1;  // bytes per element
+  FftIo io{bytes, nullptr, seq0, cin, cout, rout, lag0, 0.0, tws, tws + 64, nullptr, nullptr};
+  if (IN == FFT_IN_CENTRED || IN == FFT_IN_PAIRS_CENTRED)
+    io.mean = __ddiv_rn((double)*sum, (double)p.H * (double)p.W);
+  if constexpr ((IN == FFT_IN_BYTES || IN == FFT_IN_CENTRED || IN == FFT_IN_PAIRS || IN == FFT_IN_PAIRS_CENTRED) &&
+                N >= 16 && CTA == 256) {
+    constexpr int BPE = (IN == FFT_IN_PAIRS || IN == FFT_IN_PAIRS_CENTRED) ? 2 : 1;  // bytes per element
     __shared__ uint4 stage[CTA * BPE];                // S N BPE = CTA * 16 * BPE bytes
     if (p.rows && p.in_pitch == (uint64_t)N * BPE && (reinterpret_cast<uintptr_t>(bytes) & 15) == 0) {
       const uint64_t rows = (p.nseq - seq0 < p.S) ? p.nseq - seq0 : p.S;
@@ -398,15 +460,24 @@ __global__ void __launch_bounds__(CTA, 512 / CTA)
       io.sb = reinterpret_cast<const uint8_t*>(stage);
     }
   }
-  __shared__ double2 tw2s[OUT == FFT_OUT_R2C ? 64 + (2 * N > 64 ? 2 * N / 64 : 1) : 1];
-  if (OUT == FFT_OUT_R2C)
+  constexpr bool TW2 = OUT == FFT_OUT_R2C || IN == FFT_IN_C2R;
+  __shared__ double2 tw2s[TW2 ? 64 + (2 * N > 64 ? 2 * N / 64 : 1) : 1];
+  if (TW2)
     for (uint32_t i = threadIdx.x; i < 64 + (2 * N > 64 ? 2 * N / 64 : 0); i += CTA)
       if (i < 64) { if (i < 2u * N) tw2s[i] = __ldg(p.tw2 + i); }
       else tw2s[i] = __ldg(p.tw2 + 64 * (i - 64));
+  io.t2lo = tw2s;
+  io.t2hi = tw2s + 64;
   __syncthreads();  // twiddle tables (and the staged bytes) visible to the CTA
   double2 a[16];
   FlatAcc fa;
   fft_passes<LOGN, 0, IN, OUT>(p, io, a, Xs, tid, seq, active, valid, fa, no_prefetch);
+  if constexpr (OUT == FFT_OUT_POWER_FFT) {  // |.|^2 in shared memory, then the second transform
+    power_in_place<N>(p, Xs, tid, seq, valid);
+    __syncthreads();
+    fft_passes<LOGN, 0, FFT_IN_COMPLEX, FFT_OUT_COMPLEX, true>(p, io, a, Xs, tid, seq, active, valid, fa,
+                                                                no_prefetch);
+  }
   if constexpr (OUT == FFT_OUT_R2C) r2c_epilogue<N>(p, io, Xs, tid, seq, valid, tw2s, tw2s + 64);
   if constexpr (OUT == FFT_OUT_HALF_SPECTRUM)
     if (seq0 == 0 && s == 0 && active) half_col0_epilogue<N>(p, io, Xs, tid, fa);
