@@ -566,24 +566,22 @@ uint32_t ilog2(uint32_t v) { return 31u - (uint32_t)__builtin_clz(v); }
 // so the workspace is dense.
 uint64_t fft_ws_pitch(uint32_t W) { return W; }
 
-lz::FftPass fft_rows(uint32_t H, uint32_t W, const double2* tw, uint64_t in_pitch, uint64_t out_pitch) {
+lz::FftPass fft_rows(uint32_t H, uint32_t W, uint64_t in_pitch, uint64_t out_pitch) {
   lz::FftPass p = lz::fft_plan(W, ilog2(W), H, true);
   p.rows = 1;
   p.in_pitch = in_pitch;
   p.out_pitch = out_pitch;
   p.H = H;
   p.W = W;
-  p.tw = tw;
   return p;
 }
-lz::FftPass fft_cols(uint32_t H, uint32_t W, const double2* tw, uint64_t in_pitch, uint64_t out_pitch) {
+lz::FftPass fft_cols(uint32_t H, uint32_t W, uint64_t in_pitch, uint64_t out_pitch) {
   lz::FftPass p = lz::fft_plan(H, ilog2(H), W, false);
   p.rows = 0;
   p.in_pitch = in_pitch;
   p.out_pitch = out_pitch;
   p.H = H;
   p.W = W;
-  p.tw = tw;
   return p;
 }
 
@@ -633,11 +631,6 @@ bool fft_launch(const lz::FftPass& p, const uint8_t* bytes, const double2* cin, 
   }
 }
 
-// twiddle tables for the row (W) and column (H) lengths: tw[0..W) then tw[W..W+H)
-bool fft_twiddle(double2* tw, uint32_t n, cudaStream_t st) {
-  lz::twiddle_kernel<<<(n + 255) / 256, 256, 0, st>>>(tw, n);
-  return cuda_ok(cudaGetLastError(), "twiddles");
-}
 
 
 lorenz_status spectra_args(const uint8_t* x, uint32_t H, uint32_t W, const double* out) {
@@ -667,22 +660,16 @@ lorenz_status lorenz_power_spectrum(const uint8_t* x, uint32_t H, uint32_t W, do
   const bool r2c = W >= 4;
   const uint32_t M = r2c ? W / 2 : W;
   const uint64_t NW = (uint64_t)H * M;
-  if (!cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&ws), (NW + M + W + H) * sizeof(double2), st),
-               "alloc fft"))
+  if (!cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&ws), NW * sizeof(double2), st), "alloc fft"))
     return LORENZ_E_CUDA;
-  double2* tw_r = ws + NW;   // M-point (row FFTs)
-  double2* tw_2 = tw_r + M;  // W-point (R2C unpack)
-  double2* tw_c = tw_2 + W;  // H-point (column FFTs)
-  lz::FftPass rows = fft_rows(H, M, tw_r, W, M), cols = fft_cols(H, M, tw_c, M, W);
+  lz::FftPass rows = fft_rows(H, M, W, M), cols = fft_cols(H, M, M, W);
   rows.W = cols.W = W;
-  rows.tw2 = tw_2;
   cols.scale = std::ldexp(1.0, -2 * (int)ilog2((uint32_t)N));  // 1 / N^2
   const uint32_t tiles = (cols.nseq + cols.S - 1) / cols.S;  // >= the column pass's grid
   unsigned nparts = 0;                                          // one flatness partial per column CTA
   bool ok = !flatness ||
             cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&part), tiles * sizeof(double2), st), "alloc");
   cols.part = flatness ? part : nullptr;
-  ok = ok && fft_twiddle(tw_r, M, st) && fft_twiddle(tw_2, W, st) && fft_twiddle(tw_c, H, st);
   if (r2c)
     ok = ok &&
          fft_launch<lz::FFT_IN_PAIRS, lz::FFT_OUT_R2C>(rows, x, nullptr, ws, nullptr, nullptr, nullptr, st) &&
@@ -718,35 +705,29 @@ lorenz_status lorenz_autocorrelation(const uint8_t* x, uint32_t H, uint32_t W, d
   const bool r2c = W >= 4;
   const uint32_t M = r2c ? W / 2 : W;
   const uint64_t Pw = r2c ? M : fft_ws_pitch(W), NW = (uint64_t)H * Pw;
-  if (!cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&ws), (NW + M + W + H) * sizeof(double2), st),
-               "alloc fft") ||
+  if (!cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&ws), NW * sizeof(double2), st), "alloc fft") ||
       !cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&aux), 16, st), "alloc aux")) {
     if (ws) cudaFreeAsync(ws, st);
     return LORENZ_E_CUDA;
   }
   double* lag0 = reinterpret_cast<double*>(aux + 1);
-  double2* tw_r = ws + NW;   // M-point (row FFTs)
-  double2* tw_2 = tw_r + M;  // W-point (R2C / C2R)
-  double2* tw_c = tw_2 + W;  // H-point (column FFTs)
   const unsigned sgrid = (unsigned)std::min<uint64_t>(4ull * sm_count(), (N + lz::kFftCta - 1) / lz::kFftCta);
-  bool ok = cuda_ok(cudaMemsetAsync(aux, 0, 16, st), "memset") && fft_twiddle(tw_r, M, st) &&
-            fft_twiddle(tw_2, W, st) && fft_twiddle(tw_c, H, st);
+  bool ok = cuda_ok(cudaMemsetAsync(aux, 0, 16, st), "memset");
   if (ok) {
     lz::byte_sum_kernel<<<sgrid, lz::kFftCta, 0, st>>>(x, N, aux);
     ok = cuda_ok(cudaGetLastError(), "byte sum");
   }
   if (ok && r2c) {
-    lz::FftPass rows1 = fft_rows(H, M, tw_r, W, M), cols = fft_cols(H, M, tw_c, M, M);
-    lz::FftPass rows2 = fft_rows(H, M, tw_r, M, M);
+    lz::FftPass rows1 = fft_rows(H, M, W, M), cols = fft_cols(H, M, M, M);
+    lz::FftPass rows2 = fft_rows(H, M, M, M);
     rows1.W = cols.W = rows2.W = W;
-    rows1.tw2 = rows2.tw2 = tw_2;
     cols.packed0 = 1;
     ok = fft_launch<lz::FFT_IN_PAIRS_CENTRED, lz::FFT_OUT_R2C>(rows1, x, nullptr, ws, nullptr, aux, nullptr, st) &&
          fft_launch<lz::FFT_IN_COMPLEX, lz::FFT_OUT_POWER_FFT>(cols, nullptr, ws, ws, nullptr, nullptr, nullptr, st) &&
          fft_launch<lz::FFT_IN_C2R, lz::FFT_OUT_REAL_PAIRS>(rows2, nullptr, ws, nullptr, r, nullptr, lag0, st);
   } else if (ok) {
-    const lz::FftPass rows1 = fft_rows(H, W, tw_2, W, Pw), cols1 = fft_cols(H, W, tw_c, Pw, Pw);
-    const lz::FftPass rows2 = fft_rows(H, W, tw_2, Pw, Pw), cols2 = fft_cols(H, W, tw_c, Pw, W);
+    const lz::FftPass rows1 = fft_rows(H, W, W, Pw), cols1 = fft_cols(H, W, Pw, Pw);
+    const lz::FftPass rows2 = fft_rows(H, W, Pw, Pw), cols2 = fft_cols(H, W, Pw, W);
     ok = fft_launch<lz::FFT_IN_CENTRED, lz::FFT_OUT_COMPLEX>(rows1, x, nullptr, ws, nullptr, aux, nullptr, st) &&
          fft_launch<lz::FFT_IN_COMPLEX, lz::FFT_OUT_POWER>(cols1, nullptr, ws, ws, nullptr, nullptr, nullptr, st) &&
          fft_launch<lz::FFT_IN_COMPLEX, lz::FFT_OUT_COMPLEX>(rows2, nullptr, ws, ws, nullptr, nullptr, nullptr, st) &&

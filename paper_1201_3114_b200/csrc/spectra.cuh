@@ -57,8 +57,6 @@ struct FftPass {
   uint64_t out_pitch;   // row pitch of a complex (workspace) output
   uint32_t H, W;        // matrix shape (for the DC shift)
   double scale;         // FFT_OUT_SPECTRUM: 1 / (HW)^2 (a power of two: exact)
-  const double2* tw;    // exp(-2 pi i m / n), m < n
-  const double2* tw2;   // FFT_OUT_R2C / FFT_IN_C2R: exp(-2 pi i m / 2n), m < 2n
   uint32_t packed0;     // FFT_OUT_POWER_FFT: sequence 0 holds the packed DC + i Nyquist column
   double2* part;        // FFT_OUT_SPECTRUM (nullable): per-CTA (sum log P, sum P) over non-DC bins
 };
@@ -100,6 +98,14 @@ __device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_doub
 // analysis arithmetic with a tolerance, not part of the bit-exact cipher)
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
   return make_double2(__fma_rn(a.x, b.x, -__dmul_rn(a.y, b.y)), __fma_rn(a.x, b.y, __dmul_rn(a.y, b.x)));
+}
+
+// exp(-2 pi i m / n) from sincospi of the exact dyadic argument 2m/n (each CTA builds its own
+// 64 + n/64-entry shared tables with it; no global twiddle table)
+__device__ __forceinline__ double2 twiddle_exact(uint32_t m, uint32_t n) {
+  double sn, cs;
+  sincospi(__ddiv_rn(2.0 * m, (double)n), &sn, &cs);
+  return make_double2(cs, -sn);
 }
 
 // x * exp(-2 pi i m / 16), m a compile-time constant after unrolling: 1 and -i are free
@@ -440,8 +446,8 @@ __global__ void __launch_bounds__(CTA, 512 / CTA)
   double2* Xs = fsm + (size_t)(active ? s : 0) * p.pitch;
   __shared__ double2 tws[64 + (N > 64 ? N / 64 : 1)];
   for (uint32_t i = threadIdx.x; i < 64 + (N > 64 ? N / 64 : 0); i += CTA)
-    if (i < 64) { if (i < (uint32_t)N) tws[i] = __ldg(p.tw + i); }
-    else tws[i] = __ldg(p.tw + 64 * (i - 64));
+    if (i < 64) { if (i < (uint32_t)N) tws[i] = twiddle_exact(i, N); }
+    else tws[i] = twiddle_exact(64 * (i - 64), N);
   FftIo io{bytes, nullptr, seq0, cin, cout, rout, lag0, 0.0, tws, tws + 64, nullptr, nullptr};
   if (IN == FFT_IN_CENTRED || IN == FFT_IN_PAIRS_CENTRED)
     io.mean = __ddiv_rn((double)*sum, (double)p.H * (double)p.W);
@@ -464,8 +470,8 @@ __global__ void __launch_bounds__(CTA, 512 / CTA)
   __shared__ double2 tw2s[TW2 ? 64 + (2 * N > 64 ? 2 * N / 64 : 1) : 1];
   if (TW2)
     for (uint32_t i = threadIdx.x; i < 64 + (2 * N > 64 ? 2 * N / 64 : 0); i += CTA)
-      if (i < 64) { if (i < 2u * N) tw2s[i] = __ldg(p.tw2 + i); }
-      else tw2s[i] = __ldg(p.tw2 + 64 * (i - 64));
+      if (i < 64) { if (i < 2u * N) tw2s[i] = twiddle_exact(i, 2 * N); }
+      else tw2s[i] = twiddle_exact(64 * (i - 64), 2 * N);
   io.t2lo = tw2s;
   io.t2hi = tw2s + 64;
   __syncthreads();  // twiddle tables (and the staged bytes) visible to the CTA
@@ -532,7 +538,7 @@ __global__ void __launch_bounds__(CTA, 512 / CTA)
   const uint64_t tiles = (p.nseq + p.S - 1) / p.S;
   uint64_t tile = blockIdx.x;
   if (tile < tiles) fft_prefetch<IN, N, LOGN, CTA>(p, bytes, cin, fsm, stage, tile);
-  for (uint32_t i = threadIdx.x; i < 64 + N / 64; i += CTA) tws[i] = __ldg(p.tw + (i < 64 ? i : 64 * (i - 64)));
+  for (uint32_t i = threadIdx.x; i < 64 + N / 64; i += CTA) tws[i] = twiddle_exact(i < 64 ? i : 64 * (i - 64), N);
   FftIo io{bytes, reinterpret_cast<const uint8_t*>(stage), 0, cin, cout, rout, lag0, 0.0, tws, tws + 64};
   if (IN == FFT_IN_CENTRED) io.mean = __ddiv_rn((double)*sum, (double)p.H * (double)p.W);
   double2 a[16];
@@ -552,14 +558,6 @@ __global__ void __launch_bounds__(CTA, 512 / CTA)
   if (OUT == FFT_OUT_SPECTRUM && p.part) flat_partial<CTA>(fa, p.part);
 }
 
-// twiddle table exp(-2 pi i m / n), m < n
-__global__ void twiddle_kernel(double2* __restrict__ tw, uint32_t n) {
-  const uint32_t m = blockIdx.x * blockDim.x + threadIdx.x;
-  if (m >= n) return;
-  double s, c;
-  sincospi(__ddiv_rn(2.0 * m, (double)n), &s, &c);
-  tw[m] = make_double2(c, -s);
-}
 
 constexpr int kFftCta = 256;  // the reductions below
 
