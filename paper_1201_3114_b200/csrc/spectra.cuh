@@ -154,22 +154,31 @@ __device__ __forceinline__ uint32_t fft_pad(uint32_t i) { return i + (i >> 4); }
 struct FlatAcc {
   double sp = 0.0, mprod = 1.0;
   int esum = 0;
-  __device__ __forceinline__ void add(double P) {
-    // P = m 2^e, m in [1/2, 1): exponent field split off with integer ops for normal P >= 0;
-    // zero and subnormals take frexp (P = 0 -> m = 0: log -> -inf, geometric mean 0)
+  // P = m 2^e, m in [1/2, 1): exponent field split off with integer ops for normal P >= 0;
+  // zero and subnormals take frexp (P = 0 -> m = 0: log -> -inf, geometric mean 0)
+  __device__ __forceinline__ static double split(double P, int& e) {
     const long long b = __double_as_longlong(P);
     const int ef = (int)(b >> 52) & 0x7ff;
-    double m;
-    int e;
     if (ef != 0) {
-      m = __longlong_as_double((b & 0x800fffffffffffffLL) | 0x3fe0000000000000LL);
       e = ef - 1022;
-    } else {
-      m = frexp(P, &e);
+      return __longlong_as_double((b & 0x800fffffffffffffLL) | 0x3fe0000000000000LL);
     }
+    return frexp(P, &e);
+  }
+  __device__ __forceinline__ void add(double P) {
+    int e;
+    const double m = split(P, e);
     mprod = __dmul_rn(mprod, m);
     esum += e;
     sp = __dadd_rn(sp, P);
+  }
+  // a bin counted twice (a half-spectrum bin and its mirror): one step of each dependent chain
+  __device__ __forceinline__ void add2(double P) {
+    int e;
+    const double m = split(P, e);
+    mprod = __dmul_rn(mprod, __dmul_rn(m, m));  // m^2 >= 1/4: 16 per thread stay far from underflow
+    esum += 2 * e;
+    sp = __dadd_rn(sp, __dmul_rn(P, 2.0));      // exact doubling
   }
   __device__ __forceinline__ double sum_log() const {
     return __dadd_rn(log(mprod), __dmul_rn((double)esum, 0.69314718055994530942));
@@ -251,7 +260,7 @@ __device__ __forceinline__ void fft_store(const FftPass& p, const FftIo& io, uin
     const uint64_t i2 = (p.H - i) & (p.H - 1), j2 = p.W - j;
     io.rout[((i + p.H / 2) & (p.H - 1)) * p.W + ((j + p.W / 2) & (p.W - 1))] = P;
     io.rout[((i2 + p.H / 2) & (p.H - 1)) * p.W + ((j2 + p.W / 2) & (p.W - 1))] = P;
-    if (p.part) { acc.add(P); acc.add(P); }
+    if (p.part) acc.add2(P);
   } else {
     io.rout[i * p.W + j] = v.x;
     if ((i | j) == 0) *io.lag0 = v.x;
