@@ -155,6 +155,18 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- reference arm: the CPU oracle
+def init_dist(dev):
+    """One process per GPU over NCCL. LORENZ_DIST_BACKEND=gloo (test only) runs the same multi-rank
+    flow with host-side collectives, e.g. several ranks time-sharing one GPU: their kernels never
+    wait on each other, only the CPU collectives do."""
+    import torch.distributed as dist
+    backend = os.environ.get("LORENZ_DIST_BACKEND", "nccl")
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=dev)
+    else:
+        dist.init_process_group(backend)
+
+
 def run_reference(a):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -230,10 +242,10 @@ def run_c5(a):
     dist_on = world > 1 or "LOCAL_RANK" in os.environ  # torchrun: NCCL even at N = 1
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    dev = torch.device("cuda", local % max(1, torch.cuda.device_count()))
+    torch.cuda.set_device(dev)
     if dist_on:
-        dist.init_process_group("nccl", device_id=dev)
+        init_dist(dev)
     n, B, T = 1 << 20, 1024, a.c5_trials
     bt = sweep.Batch(rank * T, T, n, a.n_it, B, dev)
     flush = torch.empty(2 * L2_BYTES, dtype=torch.uint8, device=dev)
@@ -264,7 +276,7 @@ def run_c5(a):
     def mx(x):
         if not dist_on:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        t = torch.tensor([x], dtype=torch.float64, device=dev if dist.get_backend() == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
     ms = mx(statistics.mean(step_ms))
@@ -318,10 +330,10 @@ def main():
     dist_on = world > 1 or "LOCAL_RANK" in os.environ  # torchrun: NCCL even at N = 1
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    dev = torch.device("cuda", local % max(1, torch.cuda.device_count()))
+    torch.cuda.set_device(dev)
     if dist_on:
-        dist.init_process_group("nccl", device_id=dev)
+        init_dist(dev)
     name, n = workload(a.workload)
     B = 1024
     pw = inputs.password()
@@ -387,7 +399,7 @@ def main():
     def max_over_ranks(x: float) -> float:
         if not dist_on:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        t = torch.tensor([x], dtype=torch.float64, device=dev if dist.get_backend() == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 

@@ -51,9 +51,10 @@ def _all_gather(t: torch.Tensor, group=None) -> torch.Tensor:
         out = torch.empty(world * t.numel(), dtype=t.dtype, device=t.device)
         dist.all_gather_into_tensor(out, t.contiguous(), group=group)
         return out.view(world, -1)
-    parts = [torch.empty_like(t) for _ in range(world)]
-    dist.all_gather(parts, t.contiguous(), group=group)
-    return torch.stack(parts)
+    src = t.contiguous().cpu()  # gloo: stage through the host
+    parts = [torch.empty_like(src) for _ in range(world)]
+    dist.all_gather(parts, src, group=group)
+    return torch.stack(parts).to(t.device)
 
 
 def xor_combine(tag16: torch.Tensor, group=None) -> torch.Tensor:
@@ -67,7 +68,12 @@ def xor_combine(tag16: torch.Tensor, group=None) -> torch.Tensor:
 
 def min_combine(first_bad: torch.Tensor, group=None) -> torch.Tensor:
     """Global minimum of the ranks' first failing block (NO_BAD when none failed)."""
-    dist.all_reduce(first_bad, op=dist.ReduceOp.MIN, group=group)
+    if dist.get_backend(group) == "nccl":
+        dist.all_reduce(first_bad, op=dist.ReduceOp.MIN, group=group)
+        return first_bad
+    h = first_bad.cpu()  # gloo: stage through the host
+    dist.all_reduce(h, op=dist.ReduceOp.MIN, group=group)
+    first_bad.copy_(h)
     return first_bad
 
 

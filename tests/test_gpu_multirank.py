@@ -1,0 +1,45 @@
+"""bench.py's multi-rank flow end to end on the one GPU of this pool: torchrun with 2 ranks that
+time-share cuda:0 and exchange only through host-side gloo collectives (LORENZ_DIST_BACKEND=gloo;
+no kernel ever waits on another rank's). Checks the contract the driver's N > 1 runs rely on:
+one JSON line (rank 0), n_gpus = 2, the round trip validated on every rank, and the combined tag
+XOR identical to the single-process run (ciphertext does not depend on the rank count).
+"""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def run(cmd, env):
+    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    return lines
+
+
+@pytest.mark.parametrize("workload", ["c3", "c5"])
+def test_two_ranks_one_gpu_gloo(workload):
+    env = dict(os.environ, LORENZ_DIST_BACKEND="gloo")
+    args = ["bench.py", "--workload", workload, "--steps", "1", "--warmup", "1", "--no-cpu-baseline"]
+    if workload == "c5":
+        args += ["--c5-trials", "8"]
+    two = run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+               "--master-addr", "127.0.0.1", "--master-port", "29531" if workload == "c3" else "29532"]
+              + args + ["--gpus", "2"], env)
+    assert len(two) == 1, two  # rank 0 alone prints
+    d2 = json.loads(two[0])
+    assert d2["n_gpus"] == 2 and d2["value"] > 0 and d2["clocks"]["sm_mhz"] > 0
+    if workload == "c3":
+        assert d2["validated"]["round_trip"] is True
+        assert d2["e2e"]["matches_device_ct"] is True
+        one = run([sys.executable] + args + ["--gpus", "1"], os.environ.copy())
+        d1 = json.loads(one[-1])
+        assert d1["validated"]["tag_xor"] == d2["validated"]["tag_xor"]
+    else:
+        s = d2["c5_stats_rank0"]
+        assert s["untouched_blocks_identical"] and s["ct_entropy_min"] > 7.9
