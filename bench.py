@@ -176,7 +176,7 @@ def run_reference(a):
     name, n = workload(a.workload)
     B = 1024
     pw = inputs.password()
-    prm = oracle.params(mode=oracle.FAST, n_it=a.n_it, block_size=B)
+    prm = oracle.params(mode=oracle.FAST, n_it=a.n_it, block_size=B, integrator=ORACLE_INTEG[a.integrator])
     threads = cores()
     # calibrate: blocks per step so that warmup + steps take ~2-3 minutes in total
     probe = max(threads, 8)
@@ -202,17 +202,20 @@ def run_reference(a):
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(sec * 1e3, 3), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (SplitMix64, DESIGN.md §6)",
         "config": {"workload": name, "message_bytes": n, "block_size": B, "n_it": a.n_it, "mode": "FAST",
-                   "parallelism": f"cpu threads {threads}"},
+                   "integrator": a.integrator.upper(), "parallelism": f"cpu threads {threads}"},
         "cpu_baseline": {"value": round(mbps, 4), "unit": "MB/s", "cores": threads, "kind": "oracle",
                          "sample": sample, "cpu": cpu_model()},
         "e2e": {"value": round(mbps, 4), "unit": "MB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
 
-def cpu_baseline(pw, n_it, B, n, target_s):
+ORACLE_INTEG = {"rk4": 0, "euler": 1, "rk4fma": 2}  # oracle.RK4 / EULER / RK4_FMA
+
+
+def cpu_baseline(pw, n_it, B, n, target_s, integrator="rk4"):
     import oracle
     from paper_1201_3114_b200 import inputs
-    prm = oracle.params(mode=oracle.FAST, n_it=n_it, block_size=B)
+    prm = oracle.params(mode=oracle.FAST, n_it=n_it, block_size=B, integrator=ORACLE_INTEG[integrator])
     threads = cores()
     probe = max(threads, 8)
     msg = inputs.message(probe * B)
@@ -449,7 +452,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
-        cpu = cpu_baseline(pw, a.n_it, B, n, a.cpu_seconds)
+        cpu = cpu_baseline(pw, a.n_it, B, n, a.cpu_seconds, a.integrator)
 
     if rank == 0:
         out = {

@@ -50,6 +50,18 @@ def main():
             chis.append(round(float((((h[c, k, :100] - e) ** 2) / e).sum()), 1))
         out["coords"][name] = {"int_part_range": [int(nz.min()), int(nz.max())],
                                "chi2_digits_12_34_56": chis, "chi2_p99_99dof": 135.8}
+    # the CPU oracle beside it: the same recipe on a bounded sample of trajectories, one core
+    import time
+
+    import oracle
+    lanes_cpu = min(a.lanes, 512)
+    t0 = time.perf_counter()
+    oracle.digit_hist(inputs.initial_states(lanes_cpu), a.skip, a.samples, a.stride)
+    cpu_s = time.perf_counter() - t0
+    steps = a.skip + a.samples * a.stride
+    out["cpu_oracle"] = {"lanes": lanes_cpu, "seconds": round(cpu_s, 3), "cores": 1,
+                         "rk4_steps_per_s": round(lanes_cpu * steps / cpu_s, 1),
+                         "gpu_rk4_steps_per_s": round(a.lanes * steps / sec, 1)}
     print(json.dumps(out))
 
 

@@ -7,6 +7,7 @@ Prints JSON lines:
     unavoidable 9 N (bytes in, float64 out) and the implemented pipeline's 25 N (spectrum:
     R2C rows + half-spectrum columns) / 58 N (autocorrelation: byte sum, R2C rows, fused
     transform-|.|^2-transform columns, C2R rows, normalisation) -> GB/s;
+  * the CPU oracle (plain O(N^2) sums, one core) timed beside the GPU at --oracle-side (128);
   * the Fig.3 / Fig.4 experiment at --fig x --fig: a synthetic plain image, its ciphertext
     (FAST, the first N ciphertext bytes) and white noise -> byte entropy, spectral flatness,
     r(1,0), r(0,1), max off-origin |r|.
@@ -60,6 +61,7 @@ def main():
     ap.add_argument("--sizes", type=int, nargs="+", default=[256, 1024, 4096])
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--fig", type=int, default=1024)
+    ap.add_argument("--oracle-side", type=int, default=128)
     a = ap.parse_args()
     for s in a.sizes:
         n = s * s
@@ -74,6 +76,27 @@ def main():
                           "spectrum_gbs_in_out": round(9 * n / tp / 1e9, 1), "autocorr_ms": round(ta * 1e3, 4),
                           "autocorr_gbs_pipeline": round(58 * n / ta / 1e9, 1),
                           "autocorr_gbs_in_out": round(9 * n / ta / 1e9, 1)}))
+    if a.oracle_side:
+        import time
+
+        import oracle
+        s = a.oracle_side
+        img = inputs.message(s * s, seed=2).reshape(s, s)
+        t0 = time.perf_counter()
+        oracle.power_spectrum(img)
+        cp = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        oracle.autocorr(img)
+        ca = time.perf_counter() - t0
+        x = torch.from_numpy(img).to(DEV)
+        p = torch.empty((s, s), dtype=torch.float64, device=DEV)
+        f = torch.empty(1, dtype=torch.float64, device=DEV)
+        r = torch.empty((s, s), dtype=torch.float64, device=DEV)
+        tp = timed(lambda: L.lorenz_power_spectrum(x, p, f), a.reps)
+        ta = timed(lambda: L.lorenz_autocorrelation(x, r), a.reps)
+        print(json.dumps({"what": "CPU oracle beside the GPU (plain O(N^2) definitions, 1 core)", "side": s,
+                          "oracle_spectrum_s": round(cp, 3), "gpu_spectrum_ms": round(tp * 1e3, 4),
+                          "oracle_autocorr_s": round(ca, 3), "gpu_autocorr_ms": round(ta * 1e3, 4)}))
     s = a.fig
     n = s * s
     plain = plain_image(s, s)
