@@ -191,6 +191,23 @@ lorenz_status lorenz_digit_histograms(const double* ic, uint64_t lanes, uint32_t
                                       uint32_t stride, uint32_t dt_code, uint32_t integrator,
                                       uint64_t* hist, void* cuda_stream);
 
+/* ---- ragged batches (serving many messages of different lengths in one launch) ----
+ * `count` FAST messages, message s of n[s] plaintext bytes under keys[s] (all keys with equal
+ * params). Arrays n / *_off are HOST arrays of `count` entries; pts / cts / tags are DEVICE
+ * pointers (16-byte aligned). Message s's plaintext is at pts + pt_off[s] and its ciphertext
+ * (lorenz_ct_len(n[s]) bytes, blocks as in the single-message layout) at cts + ct_off[s]; every
+ * offset a multiple of 16; output ranges must not overlap each other or the input. tags (16*count
+ * bytes) receives each message's tag XOR (decrypt: of the received ciphertext). One launch over
+ * all blocks of all messages (a lane finds its message by binary search over the block prefix
+ * sums). Synchronous. Decrypt: first_bad (HOST, count entries) = the message's lowest failing
+ * block or -1; a failing message's plaintext is zero-filled; LORENZ_E_INTEGRITY if any failed. */
+lorenz_status lorenz_encrypt_ragged(const lorenz_key* keys, uint32_t count, const uint64_t* n,
+                                    const uint64_t* pt_off, const uint64_t* ct_off, const uint8_t* pts,
+                                    uint8_t* cts, uint8_t* tags, void* cuda_stream);
+lorenz_status lorenz_decrypt_ragged(const lorenz_key* keys, uint32_t count, const uint64_t* n,
+                                    const uint64_t* ct_off, const uint64_t* pt_off, const uint8_t* cts,
+                                    uint8_t* pts, uint8_t* tags, int64_t* first_bad, void* cuda_stream);
+
 /* ---- NEXT-4 §4 analysis: Fig.3 autocorrelation matrices and Fig.4 2-D Fourier
  * power spectra; readings Q25-Q27.
  * x: DEVICE pointer to an H x W byte matrix, row-major (e.g. the first H*W bytes of a

@@ -13,6 +13,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/lorenz.h"
@@ -528,6 +529,131 @@ lorenz_status lorenz_encrypt_batch(const lorenz_key* keys, uint32_t S, uint64_t 
     cudaStreamSynchronize(st);
   }
   return ret;
+}
+
+// ---------------------------------------------------------------- ragged batches (serving)
+}  // extern "C"
+namespace {
+// count messages of different lengths, one launch over all their blocks (DevConst.batch = 2)
+lorenz_status ragged(const lorenz_key* keys, uint32_t count, const uint64_t* n, const uint64_t* in_off,
+                     const uint64_t* out_off, const uint8_t* in, uint8_t* out, uint8_t* tags, int64_t* first_bad,
+                     bool decrypt, cudaStream_t st) {
+  if (!keys || count == 0 || count > (1u << 30) || !n || !in_off || !out_off || !in || !out || !tags ||
+      !aligned16(in) || !aligned16(out) || (decrypt && !first_bad))
+    return LORENZ_E_ARG;
+  const KeyImpl* K0 = impl(&keys[0]);
+  if (!K0 || K0->prm.mode != LORENZ_FAST) return LORENZ_E_ARG;
+  for (uint32_t s = 1; s < count; ++s) {
+    const KeyImpl* Ks = impl(&keys[s]);
+    if (!Ks || std::memcmp(&Ks->prm, &K0->prm, sizeof K0->prm) != 0) return LORENZ_E_ARG;
+  }
+  // host tables: block prefix sums, lengths, offsets; per-message extents for the overlap checks
+  std::vector<uint64_t> tab(4ull * count + 1);
+  uint64_t* blk = tab.data();
+  uint64_t *len = blk + count + 1, *ioff = len + count, *ooff = ioff + count;
+  std::vector<std::pair<uint64_t, uint64_t>> outs(count);
+  uint64_t in_end = 0, out_end = 0;
+  blk[0] = 0;
+  for (uint32_t s = 0; s < count; ++s) {
+    const uint64_t nb = nblocks(K0, n[s]), ctl = n[s] + 16 * nb;
+    if ((in_off[s] | out_off[s]) & 15) return LORENZ_E_ARG;  // 16-byte aligned message starts
+    const uint64_t ib = decrypt ? ctl : n[s], ob = decrypt ? n[s] : ctl;
+    blk[s + 1] = blk[s] + nb;
+    len[s] = n[s];
+    ioff[s] = in_off[s];
+    ooff[s] = out_off[s];
+    in_end = std::max(in_end, in_off[s] + ib);
+    out_end = std::max(out_end, out_off[s] + ob);
+    outs[s] = {out_off[s], out_off[s] + ob};
+  }
+  std::sort(outs.begin(), outs.end());
+  for (uint32_t s = 1; s < count; ++s)
+    if (outs[s].first < outs[s - 1].second && outs[s].second > outs[s].first) {
+      g_err = "ragged batch: output ranges overlap";
+      return LORENZ_E_ARG;
+    }
+  if (overlap(in, in_end, out, out_end)) return LORENZ_E_ARG;
+  const uint64_t lanes = blk[count];
+  std::vector<lz::DevKey> h_keys(count);
+  for (uint32_t s = 0; s < count; ++s) h_keys[s] = make_devkey(impl(&keys[s]));
+  keep_pool_cached();
+  lz::DevKey* d_keys = nullptr;
+  uint64_t* d_tab = nullptr;  // blk | len | in | out | bad
+  lorenz_result* d_res = nullptr;
+  lorenz_status ret = LORENZ_OK;
+  std::vector<uint64_t> bad(count, ~0ULL);
+  do {
+    if (!cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&d_keys), sizeof(lz::DevKey) * count, st), "alloc") ||
+        !cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&d_tab), 8 * (5ull * count + 1), st), "alloc")) {
+      ret = LORENZ_E_CUDA; break;
+    }
+    if (!cuda_ok(cudaMemcpyAsync(d_keys, h_keys.data(), sizeof(lz::DevKey) * count, cudaMemcpyHostToDevice, st),
+                 "keys H2D") ||
+        !cuda_ok(cudaMemcpyAsync(d_tab, tab.data(), 8 * tab.size(), cudaMemcpyHostToDevice, st), "tables H2D") ||
+        !cuda_ok(cudaMemsetAsync(d_tab + tab.size(), 0xFF, 8ull * count, st), "verdicts") ||
+        !cuda_ok(cudaMemsetAsync(tags, 0, 16ull * count, st), "tags memset")) {
+      ret = LORENZ_E_CUDA; break;
+    }
+    if ((ret = alloc_result(&d_res, st)) != LORENZ_OK) break;
+    lz::DevConst C = make_const(K0, 0, 0, lanes);
+    C.batch = 2;
+    C.count = count;
+    C.rag_blk = d_tab;
+    C.rag_len = d_tab + count + 1;
+    C.rag_in = d_tab + 2ull * count + 1;
+    C.rag_out = d_tab + 3ull * count + 1;
+    C.rag_bad = reinterpret_cast<unsigned long long*>(d_tab + 4ull * count + 1);
+    lz::DevKey dummy;
+    std::memset(&dummy, 0, sizeof dummy);
+    const cudaError_t e =
+        decrypt ? launch_chain<lz::OP_DEC>(C, dummy, d_keys, K0->prm.integrator, in, out, d_res, tags, nullptr, st)
+                : launch_chain<lz::OP_ENC>(C, dummy, d_keys, K0->prm.integrator, in, out, d_res, tags, nullptr, st);
+    if (!cuda_ok(e, "ragged launch")) { ret = LORENZ_E_CUDA; break; }
+    if (decrypt &&
+        !cuda_ok(cudaMemcpyAsync(bad.data(), C.rag_bad, 8ull * count, cudaMemcpyDeviceToHost, st), "verdicts D2H")) {
+      ret = LORENZ_E_CUDA; break;
+    }
+  } while (0);
+  if (d_keys) cudaFreeAsync(d_keys, st);
+  if (d_tab) cudaFreeAsync(d_tab, st);
+  if (d_res) {
+    lorenz_result h;
+    lorenz_status f = finish_sync(d_res, st, &h);  // synchronises the stream (verdicts are on the host)
+    if (ret == LORENZ_OK || (ret == LORENZ_E_INTEGRITY && f != LORENZ_E_INTEGRITY)) ret = f;
+  } else {
+    cudaStreamSynchronize(st);
+  }
+  if (decrypt && (ret == LORENZ_OK || ret == LORENZ_E_INTEGRITY)) {
+    bool any = false;
+    for (uint32_t s = 0; s < count; ++s) {
+      first_bad[s] = bad[s] == ~0ULL ? -1 : (int64_t)bad[s];
+      if (bad[s] != ~0ULL && n[s]) {  // never release a failing message's plaintext
+        any = true;
+        if (!cuda_ok(cudaMemsetAsync(out + out_off[s], 0, n[s], st), "zero")) ret = LORENZ_E_CUDA;
+      }
+    }
+    if (any) {
+      cudaStreamSynchronize(st);
+      if (ret == LORENZ_OK) ret = LORENZ_E_INTEGRITY;
+    }
+  }
+  return ret;
+}
+}  // namespace
+extern "C" {
+
+lorenz_status lorenz_encrypt_ragged(const lorenz_key* keys, uint32_t count, const uint64_t* n, const uint64_t* pt_off,
+                                    const uint64_t* ct_off, const uint8_t* pts, uint8_t* cts, uint8_t* tags,
+                                    void* stream) {
+  Trace tr("lorenz_encrypt_ragged");
+  return ragged(keys, count, n, pt_off, ct_off, pts, cts, tags, nullptr, false, (cudaStream_t)stream);
+}
+
+lorenz_status lorenz_decrypt_ragged(const lorenz_key* keys, uint32_t count, const uint64_t* n, const uint64_t* ct_off,
+                                    const uint64_t* pt_off, const uint8_t* cts, uint8_t* pts, uint8_t* tags,
+                                    int64_t* first_bad, void* stream) {
+  Trace tr("lorenz_decrypt_ragged");
+  return ragged(keys, count, n, ct_off, pt_off, cts, pts, tags, first_bad, true, (cudaStream_t)stream);
 }
 
 // ---------------------------------------------------------------- NEXT-4 analysis (Fig.1)

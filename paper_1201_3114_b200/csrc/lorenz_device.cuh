@@ -36,8 +36,15 @@ struct DevConst {
   uint64_t in_msg_stride, out_msg_stride;
   uint32_t n_it;                       // map iterations per character
   uint32_t fast;                       // 1: per-block sub-keys
-  uint32_t batch;                      // 1: keys from the device array, tags per message
+  uint32_t batch;                      // 1: keys from the device array, tags per message; 2: ragged
   uint32_t variant;                    // NEXT-4 Step-3 reading (0 = Q13; see lorenz.h)
+  // batch == 2 (ragged: messages of different lengths), device arrays over the `count` messages:
+  const uint64_t* rag_blk;             // block prefix sums, count + 1 entries (lane -> message)
+  const uint64_t* rag_len;             // plaintext lengths
+  const uint64_t* rag_in;              // byte offset of each message in `in`
+  const uint64_t* rag_out;             // byte offset of each message in `out`
+  unsigned long long* rag_bad;         // decrypt / verify: min failing block per message
+  uint32_t count;
 };
 
 enum { OP_ENC = 0, OP_DEC = 1, OP_VERIFY = 2 };
@@ -454,17 +461,31 @@ __global__ void __launch_bounds__(CTA, (min_ctas<INTEG, CTA>()))
   const bool active = g < C.lanes;
 
   // lane -> (message s, global block bl)
-  uint64_t s = 0, bl = C.b0 + g;
-  if (C.batch) { s = g / C.nb; bl = g - s * C.nb; }
+  uint64_t s = 0, bl = C.b0 + g, msg_n = C.n;
+  if (C.batch == 1) { s = g / C.nb; bl = g - s * C.nb; }
+  if (C.batch == 2 && active) {  // ragged: the message whose block range holds g (binary search)
+    uint32_t lo = 0, hi = C.count;
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (C.rag_blk[mid] <= g) lo = mid; else hi = mid;
+    }
+    s = lo;
+    bl = g - C.rag_blk[lo];
+    msg_n = C.rag_len[lo];
+  }
   uint64_t len = 0;
   if (active) {
     const uint64_t start = C.fast ? bl * C.B : 0;
-    len = C.fast ? ((C.n - start) < C.B ? (C.n - start) : C.B) : C.n;
+    len = C.fast ? ((msg_n - start) < C.B ? (msg_n - start) : C.B) : msg_n;
   }
   const uint64_t total = active ? len + 16 : 0;
   const uint64_t rb = bl - C.b0;  // block index inside the slice
   const uint8_t* irow = in + s * C.in_msg_stride + rb * (OP == OP_ENC ? C.B : C.B + 16);
   uint8_t* orow = out + s * C.out_msg_stride + rb * (OP == OP_ENC ? C.B + 16 : C.B);
+  if (C.batch == 2) {
+    irow = in + (active ? C.rag_in[s] : 0) + bl * (OP == OP_ENC ? C.B : C.B + 16);
+    orow = out + (active ? C.rag_out[s] : 0) + bl * (OP == OP_ENC ? C.B + 16 : C.B);
+  }
   if (!active) { irow = in; orow = out; }
 
   Chain ch;
@@ -583,6 +604,7 @@ __global__ void __launch_bounds__(CTA, (min_ctas<INTEG, CTA>()))
     if (OP != OP_ENC) {
       if (bad) {
         atomicMin((unsigned long long*)&res->first_bad, (unsigned long long)bl);
+        if (C.batch == 2) atomicMin(C.rag_bad + s, (unsigned long long)bl);
         atomicOr(&res->status, (uint32_t)ST_INTEGRITY);
         if (OP == OP_DEC)  // never release unauthenticated plaintext
           for (uint64_t j = 0; j < len; ++j) orow[j] = 0;

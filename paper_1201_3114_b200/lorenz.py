@@ -30,7 +30,7 @@ EXPORTS = ["lorenz_abi_version", "lorenz_last_error", "lorenz_status_string", "l
            "lorenz_encrypt_batch", "lorenz_encrypt_host", "lorenz_decrypt_host",
            "lorenz_compare_spans", "lorenz_histograms", "lorenz_envelope_write", "lorenz_envelope_read",
            "lorenz_encrypt_file", "lorenz_decrypt_file", "lorenz_digit_histograms",
-           "lorenz_autocorrelation", "lorenz_power_spectrum"]
+           "lorenz_autocorrelation", "lorenz_power_spectrum", "lorenz_encrypt_ragged", "lorenz_decrypt_ragged"]
 E_IO, E_FORMAT = 7, 8
 ENVELOPE_BYTES = 24
 
@@ -97,6 +97,8 @@ def lib():
         L.lorenz_decrypt_async.argtypes = [kp, u64, u64, u64, vp, vp, vp, vp, vp]
         L.lorenz_verify_async.argtypes = [kp, u64, u64, u64, vp, vp, vp]
         L.lorenz_encrypt_batch.argtypes = [kp, u32, u64, vp, vp, vp, vp]
+        L.lorenz_encrypt_ragged.argtypes = [kp, u32, vp, vp, vp, vp, vp, vp, vp]
+        L.lorenz_decrypt_ragged.argtypes = [kp, u32, vp, vp, vp, vp, vp, vp, vp, vp]
         L.lorenz_compare_spans.argtypes = [vp, vp, C.POINTER(lorenz_span), u32, vp, vp]
         L.lorenz_histograms.argtypes = [vp, C.POINTER(lorenz_span), u32, vp, vp]
         L.lorenz_digit_histograms.argtypes = [vp, u64, u32, u32, u32, u32, u32, vp, vp]
@@ -239,6 +241,33 @@ def lorenz_encrypt_batch(keys: list[Key], n: int, pts, cts, tags, stream=None):
     arr = (lorenz_key * len(keys))(*[k.raw for k in keys])
     _check(lib().lorenz_encrypt_batch(arr, len(keys), n, _ptr(pts), _ptr(cts), _ptr(tags), _stream(stream)),
            "lorenz_encrypt_batch")
+
+
+def _u64(xs):
+    import numpy as np
+    return np.ascontiguousarray(np.asarray(xs, dtype=np.uint64))
+
+
+def lorenz_encrypt_ragged(keys: list[Key], n, pt_off, ct_off, pts, cts, tags, stream=None):
+    """Ragged batch: message s (n[s] bytes, keys[s]) at pts + pt_off[s] -> cts + ct_off[s]; tags
+    device uint8[16 * len(keys)]. n / offsets: host sequences (offsets multiples of 16)."""
+    arr = (lorenz_key * len(keys))(*[k.raw for k in keys])
+    nn, po, co = _u64(n), _u64(pt_off), _u64(ct_off)
+    _check(lib().lorenz_encrypt_ragged(arr, len(keys), nn.ctypes.data, po.ctypes.data, co.ctypes.data, _ptr(pts),
+                                       _ptr(cts), _ptr(tags), _stream(stream)), "lorenz_encrypt_ragged")
+
+
+def lorenz_decrypt_ragged(keys: list[Key], n, ct_off, pt_off, cts, pts, tags, stream=None):
+    """Returns (status, first_bad: list of per-message lowest failing block or -1)."""
+    import numpy as np
+    arr = (lorenz_key * len(keys))(*[k.raw for k in keys])
+    nn, co, po = _u64(n), _u64(ct_off), _u64(pt_off)
+    fb = np.full(len(keys), -1, dtype=np.int64)
+    st = lib().lorenz_decrypt_ragged(arr, len(keys), nn.ctypes.data, co.ctypes.data, po.ctypes.data, _ptr(cts),
+                                     _ptr(pts), _ptr(tags), fb.ctypes.data, _stream(stream))
+    if st not in (OK, E_INTEGRITY):
+        raise LorenzError(st, "lorenz_decrypt_ragged")
+    return st, fb.tolist()
 
 
 def _spans(spans) -> tuple:
