@@ -59,6 +59,12 @@ def parse():
     return ap.parse_args()
 
 
+def kernel_label(plan: dict, integrator: str) -> str:
+    """Name of the chain kernel the library launches for this plan (lorenz_launch_plan)."""
+    kern = "lorenz_chain_seg_kernel" if plan["kind"] == "balanced" else "lorenz_chain_kernel"
+    return f"lz::{kern}<ENC,{integrator.upper()},{plan['cta']}>"
+
+
 def workload(name: str):
     if name == "c3":
         return "C3: 64 MiB message, FAST, B=1024, on 1 B200", 64 << 20
@@ -413,6 +419,7 @@ def main():
     value = n / (ms_step / 1e3) / 1e6
     dec_value = n / (dec_sum / a.steps / 1e3) / 1e6
 
+    plan = L.lorenz_launch_plan(key, n, b0, b1)
     # roofline: the chain kernel's algorithmic FP64 ops per launch / its event time (this rank)
     ops = fp64_ops(n, B, b0, b1, a.n_it, a.integrator)
     kern_s = statistics.mean(enc_kernel_ms) / 1e3  # result init + chain kernel on the launching stream
@@ -466,7 +473,7 @@ def main():
             "decrypt": {"value": round(dec_value, 3), "unit": "MB/s", "ms_per_step": round(dec_sum / a.steps, 3)},
             "roofline": {"bound": "alu", "achieved": round(achieved, 4), "peak": round(peak, 4), "unit": "TFLOP/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic,
-                         "kernel": f"lz::lorenz_chain_kernel<ENC,{a.integrator.upper()}>",
+                         "kernel": kernel_label(plan, a.integrator), "schedule": plan,
                          "ops_per_launch": ops, "peak_basis": "148 SM x 64 FP64 lanes x sm_max_mhz (DESIGN.md §4)",
                          "hbm_gbs": round((sl.pt_bytes + sl.ct_bytes) / kern_s / 1e9, 3),
                          "kernel_ms": round(kern_s * 1e3, 3)},

@@ -110,6 +110,25 @@ uint64_t lorenz_num_blocks(const lorenz_key* k, uint64_t n);
 uint64_t lorenz_ct_len(const lorenz_key* k, uint64_t n);
 /* Inverse of lorenz_ct_len; LORENZ_E_LENGTH if no n maps to ct_len. */
 lorenz_status lorenz_pt_len(const lorenz_key* k, uint64_t ct_len, uint64_t* n_out);
+/* Launch plan of the chain kernel for global blocks [b0, b1) of an n-byte message (host
+ * only, no device work; uses the current device's SM count, 148 without a device).
+ * kind 0 = wave kernel: one lane per block, one warp per 32 blocks, grid = ceil(lanes / cta).
+ * kind 1 = balanced kernel: grid = one CTA of `cta` threads per SM; the
+ * lanes' 32-block units, (B+16)/16 chunks each, are dealt to `slots` resident warps,
+ * `chunks_per_slot` chunks each, a unit cut by a slot boundary handing its chain states
+ * from one warp to the next. Chooses exactly as the encrypt/decrypt/verify calls do
+ * (LORENZ_SCHED / LORENZ_SEG_SLOTS overrides included). LORENZ_E_ARG on a NULL or bad
+ * key/out or an out-of-range block range. */
+typedef struct {
+  uint32_t kind;            /* 0 wave, 1 balanced                                     */
+  uint32_t cta;             /* threads per CTA                                        */
+  uint64_t grid;            /* CTAs                                                   */
+  uint64_t lanes;           /* b1 - b0 chains                                         */
+  uint64_t slots;           /* balanced: warp slots sharing the units (0 for wave)    */
+  uint64_t chunks_per_slot; /* balanced: 16-character chunks per slot (0 for wave)    */
+} lorenz_plan;
+lorenz_status lorenz_launch_plan(const lorenz_key* k, uint64_t n, uint64_t b0, uint64_t b1,
+                                 lorenz_plan* out);
 const char* lorenz_status_string(lorenz_status s);
 const char* lorenz_last_error(void);
 int lorenz_abi_version(void);

@@ -174,11 +174,91 @@ cudaError_t launch_chain_cta(const lz::DevConst& C, const lz::DevKey& K, const l
   return cudaGetLastError();
 }
 
+void keep_pool_cached();
+
+// Balanced schedule (lz::lorenz_chain_seg_kernel, lorenz_device.cuh) for RK4 / Euler launches
+// with two or more warps of chains per SM sub-partition and fewer than three waves (rules
+// below): one CTA of 128 w threads per SM,
+// S = SMs x 4 x w warp slots, w = min(4, warps per sub-partition) (tools/tune.py: 2 warps per
+// sub-partition already keep the FP64 pipe 97 % busy, 4 reach 98 %). One CTA per SM because
+// the warp schedulers favour the older of two co-resident CTAs (tools/seg_trace.py: with
+// 2 x 256 threads per SM the second CTA's warps ran at half rate until the first finished, and
+// slots cut across the two classes waited), while the warps of one CTA keep within ~3 %.
+// Overrides for tests and tuning: LORENZ_SCHED=wave|seg, LORENZ_SEG_SLOTS=S (clamped to U).
+bool seg_plan(const lz::DevConst& C, uint32_t integrator, lz::SegPlan* P, int* cta) {
+  if (integrator != LORENZ_RK4 && integrator != LORENZ_EULER) return false;
+  const char* sched = std::getenv("LORENZ_SCHED");
+  if (sched && std::strcmp(sched, "wave") == 0) return false;
+  const uint64_t U = (C.lanes + 31) / 32, sms = (uint64_t)sm_count();
+  const bool forced = sched && std::strcmp(sched, "seg") == 0;
+  uint64_t w = std::min<uint64_t>(4, U / (4 * sms));
+  if (!forced) {
+    // The wave kernel wins (tools/tune.py, RK4): with >= 3 waves of 16 warps
+    // per SM, where the dynamic CTA dispatch balances the SMs (97.6-97.9 % of the FP64 pipe
+    // against 97.0-97.2 % here), and in one wave whose warps split evenly over the SM
+    // sub-partitions (2 per sub-partition per 256-thread CTA).
+    if (w < 2 || U > 3 * 16 * sms) return false;
+    if (U <= 16 * sms) {
+      const uint64_t per_smsp_max = 2 * ((((U + 7) / 8) + sms - 1) / sms);
+      if (100 * U >= 99 * 4 * sms * per_smsp_max) return false;
+    }
+  }
+  if (w < 2) w = 2;
+  uint64_t S = 4 * w * sms;
+  if (const char* f = std::getenv("LORENZ_SEG_SLOTS")) {
+    const uint64_t v = std::strtoull(f, nullptr, 10);
+    if (v) S = v;
+  }
+  if (S > U) S = U;
+  P->units = U;
+  P->q = (uint32_t)((C.B + 16 + 15) / 16);
+  P->slots = (uint32_t)S;
+  P->cq = (U * P->q + S - 1) / S;
+  *cta = (int)(128 * w);
+  return true;
+}
+
+template <int OP, int INTEG, int CTA>
+cudaError_t launch_seg(const lz::DevConst& C, const lz::SegPlan& P, const lz::DevKey& K, const lz::DevKey* Kb,
+                       const uint8_t* in, uint8_t* out, lorenz_result* res, uint8_t* tags, uint8_t* block_ok,
+                       cudaStream_t st) {
+  const size_t hdr = (4 * ((size_t)P.slots + 2) + 15) & ~(size_t)15;  // ticket + S + 1 flags
+  const size_t bytes = hdr + ((size_t)P.slots + 1) * lz::kSegWords * 32 * 8;
+  uint8_t* scr = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&scr), bytes, st);
+  if (e != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(scr, 0, hdr, st)) == cudaSuccess) {
+    uint32_t* ticket = reinterpret_cast<uint32_t*>(scr);
+    const unsigned grid = (unsigned)((P.slots + CTA / 32 - 1) / (CTA / 32));
+    lz::lorenz_chain_seg_kernel<OP, INTEG, CTA><<<grid, CTA, 0, st>>>(
+        C, K, Kb, in, out, res, tags, block_ok, P, ticket, ticket + 1, reinterpret_cast<uint64_t*>(scr + hdr));
+    e = cudaGetLastError();
+  }
+  const cudaError_t f = cudaFreeAsync(scr, st);
+  return e != cudaSuccess ? e : f;
+}
+
+template <int OP, int INTEG>
+cudaError_t launch_seg_cta(const lz::DevConst& C, const lz::SegPlan& P, int cta, const lz::DevKey& K,
+                           const lz::DevKey* Kb, const uint8_t* in, uint8_t* out, lorenz_result* res, uint8_t* tags,
+                           uint8_t* block_ok, cudaStream_t st) {
+  keep_pool_cached();
+  return cta == 512   ? launch_seg<OP, INTEG, 512>(C, P, K, Kb, in, out, res, tags, block_ok, st)
+         : cta == 384 ? launch_seg<OP, INTEG, 384>(C, P, K, Kb, in, out, res, tags, block_ok, st)
+                      : launch_seg<OP, INTEG, 256>(C, P, K, Kb, in, out, res, tags, block_ok, st);
+}
+
 template <int OP>
 cudaError_t launch_chain(const lz::DevConst& C, const lz::DevKey& K, const lz::DevKey* Kb,
                          uint32_t integrator, const uint8_t* in, uint8_t* out, lorenz_result* res,
                          uint8_t* tags, uint8_t* block_ok, cudaStream_t st) {
   if (C.lanes == 0) return cudaSuccess;
+  lz::SegPlan P;
+  int scta = 0;
+  if (seg_plan(C, integrator, &P, &scta))
+    return integrator == LORENZ_EULER
+               ? launch_seg_cta<OP, LORENZ_EULER>(C, P, scta, K, Kb, in, out, res, tags, block_ok, st)
+               : launch_seg_cta<OP, LORENZ_RK4>(C, P, scta, K, Kb, in, out, res, tags, block_ok, st);
   const int cta = chain_cta(C.lanes, integrator);
   if (integrator == LORENZ_RK4_FMA)
     return launch_chain_cta<OP, LORENZ_RK4_FMA, 128>(C, K, Kb, in, out, res, tags, block_ok, st);
@@ -253,6 +333,13 @@ void set_last_error(const std::string& s) { g_err = s; }  // shared with lorenz_
 
 // ======================================================================== C ABI
 extern "C" {
+
+#ifdef LZ_SEG_TRACE
+// Tuning builds only: copy the last balanced launch's per-slot timeline (4096 x 8 u64).
+int lorenz_debug_seg_trace(unsigned long long* host) {
+  return cudaMemcpyFromSymbol(host, lz::g_seg_trace, sizeof lz::g_seg_trace) == cudaSuccess ? 0 : 1;
+}
+#endif
 
 int lorenz_abi_version(void) { return LORENZ_ABI_VERSION; }
 
@@ -329,6 +416,28 @@ lorenz_status lorenz_key_params(const lorenz_key* k, lorenz_params* out) {
   const KeyImpl* K = impl(k);
   if (!K || !out) return LORENZ_E_ARG;
   *out = K->prm;
+  return LORENZ_OK;
+}
+
+lorenz_status lorenz_launch_plan(const lorenz_key* k, uint64_t n, uint64_t b0, uint64_t b1, lorenz_plan* out) {
+  const KeyImpl* K = impl(k);
+  if (!K || !out || b0 > b1 || b1 > nblocks(K, n)) return LORENZ_E_ARG;
+  std::memset(out, 0, sizeof *out);
+  const lz::DevConst C = make_const(K, n, b0, b1 - b0);
+  out->lanes = C.lanes;
+  if (C.lanes == 0) return LORENZ_OK;
+  lz::SegPlan P;
+  int cta = 0;
+  if (seg_plan(C, K->prm.integrator, &P, &cta)) {
+    out->kind = 1;
+    out->cta = (uint32_t)cta;
+    out->grid = (P.slots + cta / 32 - 1) / (cta / 32);
+    out->slots = P.slots;
+    out->chunks_per_slot = P.cq;
+  } else {
+    out->cta = (uint32_t)chain_cta(C.lanes, K->prm.integrator);
+    out->grid = (C.lanes + out->cta - 1) / out->cta;
+  }
   return LORENZ_OK;
 }
 

@@ -294,9 +294,22 @@ __device__ __forceinline__ void key_schedule(const DevKey& K, bool fast, uint32_
 
 // n_it steps of the Lorenz map. RK4 in the canonical order of DESIGN.md §2
 // (43 DADD + 32 DMUL per step, no FMA), or forward Euler (NEXT-1).
-template <int INTEG>
+// PIN (the balanced kernel): pass the six constants through an opaque x + 0.0 (exact: all are
+// positive) once per character, so they sit in registers for the loop. Without it ptxas
+// re-reads them from the constant bank inside the RK4 loop of that kernel's cut-unit paths
+// (3 LDCU.128 per step, 81 instead of 78 instructions); the wave kernel keeps them in uniform
+// registers by itself.
+template <int INTEG, bool PIN = false>
 __device__ __forceinline__ void integrate(double& x, double& y, double& z, const DevConst& C) {
-  const double S = C.sigma, R = C.rho, Bt = C.beta, h = C.h, h2 = C.h2, h6 = C.h6;
+  double S = C.sigma, R = C.rho, Bt = C.beta, h = C.h, h2 = C.h2, h6 = C.h6;
+  if (PIN) {
+    asm volatile("add.rn.f64 %0, %0, 0d0000000000000000;" : "+d"(S));
+    asm volatile("add.rn.f64 %0, %0, 0d0000000000000000;" : "+d"(R));
+    asm volatile("add.rn.f64 %0, %0, 0d0000000000000000;" : "+d"(Bt));
+    asm volatile("add.rn.f64 %0, %0, 0d0000000000000000;" : "+d"(h));
+    asm volatile("add.rn.f64 %0, %0, 0d0000000000000000;" : "+d"(h2));
+    asm volatile("add.rn.f64 %0, %0, 0d0000000000000000;" : "+d"(h6));
+  }
 #pragma unroll 1
   for (uint32_t it = 0; it < C.n_it; ++it) {
     if (INTEG == LORENZ_RK4) {
@@ -359,7 +372,7 @@ __device__ __forceinline__ void integrate(double& x, double& y, double& z, const
 
 // Steps 2-3 after the character's plaintext byte p is known (Q13).
 // Returns false if the guard of Q18 fails.
-template <int INTEG>
+template <int INTEG, bool PIN = false>
 __device__ __forceinline__ bool advance(Chain& ch, uint32_t p, const DevConst& C, const double* theta_tab) {
   // Step 2: Theta = P_i / 10^{3+Omega_3} (correctly rounded, Q19; from the per-CTA table of
   // __ddiv_rn quotients) added to r[mu_3]
@@ -368,7 +381,7 @@ __device__ __forceinline__ bool advance(Chain& ch, uint32_t p, const DevConst& C
   ch.x = ch.mu3 == 0 ? t : ch.x;
   ch.y = ch.mu3 == 1 ? t : ch.y;
   ch.z = ch.mu3 == 2 ? t : ch.z;
-  integrate<INTEG>(ch.x, ch.y, ch.z, C);
+  integrate<INTEG, PIN>(ch.x, ch.y, ch.z, C);
   const bool ok = in_guard_box(ch.x, ch.y, ch.z);
   const uint32_t order = C.variant & 3;  // warp-uniform
   if (order == LORENZ_V_LITERAL) {
@@ -439,31 +452,23 @@ constexpr int min_ctas() {
   return INTEG == LORENZ_RK4_FMA ? 5 : (LZ_MIN_CTAS > 1 ? LZ_MIN_CTAS : 512 / CTA);
 }
 
-// ------------------------------------------------------------------ the kernel
-// OP: OP_ENC / OP_DEC / OP_VERIFY; CTA: 128 or 256 threads. One lane per block; warps are
-// independent (only __syncwarp), so the CTA never waits on its slowest warp.
-template <int OP, int INTEG, int CTA>
-__global__ void __launch_bounds__(CTA, (min_ctas<INTEG, CTA>()))
-    lorenz_chain_kernel(const DevConst C, const DevKey K1, const DevKey* __restrict__ Kb,
-                        const uint8_t* __restrict__ in, uint8_t* __restrict__ out,
-                        lorenz_result* __restrict__ res, uint8_t* __restrict__ tags_batch,
-                        uint8_t* __restrict__ block_ok) {
-  constexpr int WIN = CTA >= 512 ? 32 : kWin;  // 512-thread CTAs: shorter windows keep smem < 48 KB
-  constexpr int ROW = WIN + 16, CHUNKS = WIN / 16;
-  __shared__ __align__(16) uint8_t stage[(CTA / 32) * 32 * ROW];
-  __shared__ double theta_tab[6 * 256];  // RN(p / 10^{3+e}), e = Omega_3 in [0,6), p a byte
-  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint8_t* wst = stage + warp * 32 * ROW;
-  for (uint32_t i = threadIdx.x; i < 6 * 256; i += CTA)
-    theta_tab[i] = __ddiv_rn(__uint2double_rn(i & 255), pow10_theta(3 + (i >> 8)));
-  __syncthreads();  // the only CTA-wide barrier; warps run independently afterwards
-  const uint64_t g = (uint64_t)blockIdx.x * CTA + threadIdx.x;
-  const bool active = g < C.lanes;
+// ------------------------------------------------------------------ per-lane pieces
+// Where lane g of a launch reads and writes: message s, global block bl, block rb inside
+// the slice, the lane's input/output rows, and its character count (block + sentinel).
+struct LaneIO {
+  const uint8_t* irow;
+  uint8_t* orow;
+  uint64_t s, bl, rb, len, total;  // total = len + 16 characters; 0 for an inactive lane
+  bool active;
+};
 
-  // lane -> (message s, global block bl)
+template <int OP>
+__device__ __forceinline__ LaneIO lane_io(const DevConst& C, const uint8_t* in, uint8_t* out, uint64_t g) {
+  LaneIO io;
+  io.active = g < C.lanes;
   uint64_t s = 0, bl = C.b0 + g, msg_n = C.n;
   if (C.batch == 1) { s = g / C.nb; bl = g - s * C.nb; }
-  if (C.batch == 2 && active) {  // ragged: the message whose block range holds g (binary search)
+  if (C.batch == 2 && io.active) {  // ragged: the message whose block range holds g (binary search)
     uint32_t lo = 0, hi = C.count;
     while (hi - lo > 1) {
       const uint32_t mid = (lo + hi) >> 1;
@@ -474,41 +479,51 @@ __global__ void __launch_bounds__(CTA, (min_ctas<INTEG, CTA>()))
     msg_n = C.rag_len[lo];
   }
   uint64_t len = 0;
-  if (active) {
+  if (io.active) {
     const uint64_t start = C.fast ? bl * C.B : 0;
     len = C.fast ? ((msg_n - start) < C.B ? (msg_n - start) : C.B) : msg_n;
   }
-  const uint64_t total = active ? len + 16 : 0;
-  const uint64_t rb = bl - C.b0;  // block index inside the slice
-  const uint8_t* irow = in + s * C.in_msg_stride + rb * (OP == OP_ENC ? C.B : C.B + 16);
-  uint8_t* orow = out + s * C.out_msg_stride + rb * (OP == OP_ENC ? C.B + 16 : C.B);
+  io.s = s;
+  io.bl = bl;
+  io.len = len;
+  io.total = io.active ? len + 16 : 0;
+  io.rb = bl - C.b0;
+  io.irow = in + s * C.in_msg_stride + io.rb * (OP == OP_ENC ? C.B : C.B + 16);
+  io.orow = out + s * C.out_msg_stride + io.rb * (OP == OP_ENC ? C.B + 16 : C.B);
   if (C.batch == 2) {
-    irow = in + (active ? C.rag_in[s] : 0) + bl * (OP == OP_ENC ? C.B : C.B + 16);
-    orow = out + (active ? C.rag_out[s] : 0) + bl * (OP == OP_ENC ? C.B + 16 : C.B);
+    io.irow = in + (io.active ? C.rag_in[s] : 0) + bl * (OP == OP_ENC ? C.B : C.B + 16);
+    io.orow = out + (io.active ? C.rag_out[s] : 0) + bl * (OP == OP_ENC ? C.B + 16 : C.B);
   }
-  if (!active) { irow = in; orow = out; }
+  if (!io.active) { io.irow = in; io.orow = out; }
+  return io;
+}
 
-  Chain ch;
-  if (active) {
-    const DevKey& K = C.batch ? Kb[s] : K1;
-    key_schedule(K, C.fast != 0, (uint32_t)bl, C.variant, ch);
-  }
+// What a lane accumulates over its characters besides the chain itself.
+struct LaneAcc {
+  uint64_t tlo, thi;  // last 16 ciphertext bytes = the block tag
+  bool guard_ok, bad;
+};
 
-  bool guard_ok = true, bad = false;
-  uint64_t tlo = 0, thi = 0;  // last 16 ciphertext bytes = the block tag
-  const uint64_t wtotal = warp_max_u64(total);
-
-  for (uint64_t w0 = 0; w0 < wtotal; w0 += WIN) {
+// Characters [c0, c1) of every lane of the warp: stage in, run the chain, stage out, one
+// WIN-character window at a time. c0 is a multiple of 16; c1 is a multiple of 16 or at
+// least every lane's total. Lanes stop at their own total. Warp-uniform control flow.
+template <int OP, int INTEG, int WIN, bool PIN = false>
+__device__ __forceinline__ void run_chars(const DevConst& C, const LaneIO& io, Chain& ch, LaneAcc& acc,
+                                          uint8_t* wst, const double* theta_tab, uint64_t c0, uint64_t c1,
+                                          uint32_t lane) {
+  constexpr int ROW = WIN + 16, CHUNKS = WIN / 16;
+  for (uint64_t w0 = c0; w0 < c1; w0 += WIN) {
+    const uint64_t wlim = (w0 + WIN < c1) ? w0 + WIN : c1;  // this window's end inside [c0, c1)
     // ---- stage in: 32 rows x WIN bytes, coalesced 16-B chunks ----
 #pragma unroll
     for (int it = 0; it < CHUNKS; ++it) {
       const uint32_t q = it * 32 + lane, row = q / CHUNKS, c = q % CHUNKS;
-      const uint8_t* r_in = (const uint8_t*)__shfl_sync(0xffffffffu, (unsigned long long)irow, row);
-      const uint64_t r_len = __shfl_sync(0xffffffffu, len, row);
-      const uint64_t r_tot = __shfl_sync(0xffffffffu, total, row);
+      const uint8_t* r_in = (const uint8_t*)__shfl_sync(0xffffffffu, (unsigned long long)io.irow, row);
+      const uint64_t r_len = __shfl_sync(0xffffffffu, io.len, row);
+      const uint64_t r_tot = __shfl_sync(0xffffffffu, io.total, row);
       const uint64_t pos = w0 + 16 * c;
       uint4 v = make_uint4(0, 0, 0, 0);
-      if (pos < r_tot) {
+      if (pos < r_tot && pos < wlim) {
         const uint64_t r_src = (OP == OP_ENC) ? r_len : r_tot;  // bytes readable from memory
         if (pos + 16 <= r_src) {
           v = ld_stream(r_in + pos);
@@ -532,9 +547,9 @@ __global__ void __launch_bounds__(CTA, (min_ctas<INTEG, CTA>()))
     }
     __syncwarp();
 
-    // ---- the chain over this lane's characters [w0, min(w0+WIN, total)) ----
-    if (w0 < total) {
-      const uint64_t wend = (w0 + WIN < total) ? w0 + WIN : total;
+    // ---- the chain over this lane's characters [w0, min(wlim, total)) ----
+    if (w0 < io.total) {
+      const uint64_t wend = (wlim < io.total) ? wlim : io.total;
       for (uint64_t j0 = w0; j0 < wend; j0 += 16) {
         uint4* cell = reinterpret_cast<uint4*>(wst + lane * ROW + (j0 - w0));
         const uint4 v = *cell;
@@ -553,14 +568,14 @@ __global__ void __launch_bounds__(CTA, (min_ctas<INTEG, CTA>()))
             yout = (xin + ks) & 0xFF; p = xin; cbyte = yout;
           } else {
             yout = (xin - ks) & 0xFF; p = yout; cbyte = xin;
-            if (j >= len) bad |= (yout != sent_byte((uint32_t)(j - len)));
+            if (j >= io.len) acc.bad |= (yout != sent_byte((uint32_t)(j - io.len)));
           }
           olo = (olo >> 8) | (ohi << 56);
           ohi = (ohi >> 8) | ((uint64_t)yout << 56);
-          tlo = (tlo >> 8) | (thi << 56);
-          thi = (thi >> 8) | ((uint64_t)cbyte << 56);
-          if (j + 1 == total) break;  // the last character is not advanced (Q20)
-          guard_ok &= advance<INTEG>(ch, p, C, theta_tab);
+          acc.tlo = (acc.tlo >> 8) | (acc.thi << 56);
+          acc.thi = (acc.thi >> 8) | ((uint64_t)cbyte << 56);
+          if (j + 1 == io.total) break;  // the last character is not advanced (Q20)
+          acc.guard_ok &= advance<INTEG, PIN>(ch, p, C, theta_tab);
         }
         if (cnt < 16) {  // left-align a partial chunk
           const uint32_t sh = 8 * (16 - cnt);
@@ -577,12 +592,12 @@ __global__ void __launch_bounds__(CTA, (min_ctas<INTEG, CTA>()))
 #pragma unroll
       for (int it = 0; it < CHUNKS; ++it) {
         const uint32_t q = it * 32 + lane, row = q / CHUNKS, c = q % CHUNKS;
-        uint8_t* r_out = (uint8_t*)__shfl_sync(0xffffffffu, (unsigned long long)orow, row);
-        const uint64_t r_len = __shfl_sync(0xffffffffu, len, row);
-        const uint64_t r_tot = __shfl_sync(0xffffffffu, total, row);
+        uint8_t* r_out = (uint8_t*)__shfl_sync(0xffffffffu, (unsigned long long)io.orow, row);
+        const uint64_t r_len = __shfl_sync(0xffffffffu, io.len, row);
+        const uint64_t r_tot = __shfl_sync(0xffffffffu, io.total, row);
         const uint64_t r_dst = (OP == OP_ENC) ? r_tot : r_len;
         const uint64_t pos = w0 + 16 * c;
-        if (r_tot && pos < r_dst) {
+        if (r_tot && pos < r_dst && pos < wlim) {
           const uint4 v = *reinterpret_cast<const uint4*>(wst + row * ROW + 16 * c);
           if (pos + 16 <= r_dst) {
             st_stream(r_out + pos, v);
@@ -597,28 +612,34 @@ __global__ void __launch_bounds__(CTA, (min_ctas<INTEG, CTA>()))
     }
     __syncwarp();
   }
+}
 
-  // ---- per-block verdicts and the tag combine ----
-  if (active) {
-    if (!guard_ok) atomicOr(&res->status, (uint32_t)ST_DIVERGENCE);
+// Per-block verdicts and the tag combine once a warp's lanes have run their last character.
+template <int OP>
+__device__ __forceinline__ void finish_lanes(const DevConst& C, const LaneIO& io, LaneAcc acc,
+                                             lorenz_result* __restrict__ res, uint8_t* __restrict__ tags_batch,
+                                             uint8_t* __restrict__ block_ok, uint32_t lane) {
+  if (io.active) {
+    if (!acc.guard_ok) atomicOr(&res->status, (uint32_t)ST_DIVERGENCE);
     if (OP != OP_ENC) {
-      if (bad) {
-        atomicMin((unsigned long long*)&res->first_bad, (unsigned long long)bl);
-        if (C.batch == 2) atomicMin(C.rag_bad + s, (unsigned long long)bl);
+      if (acc.bad) {
+        atomicMin((unsigned long long*)&res->first_bad, (unsigned long long)io.bl);
+        if (C.batch == 2) atomicMin(C.rag_bad + io.s, (unsigned long long)io.bl);
         atomicOr(&res->status, (uint32_t)ST_INTEGRITY);
         if (OP == OP_DEC)  // never release unauthenticated plaintext
-          for (uint64_t j = 0; j < len; ++j) orow[j] = 0;
+          for (uint64_t j = 0; j < io.len; ++j) io.orow[j] = 0;
       }
-      if (block_ok) block_ok[rb] = bad ? 0 : 1;
+      if (block_ok) block_ok[io.rb] = acc.bad ? 0 : 1;
     }
   }
   if (C.batch) {
-    if (active) {
-      unsigned long long* t = reinterpret_cast<unsigned long long*>(tags_batch + 16 * s);
-      atomicXor(t, (unsigned long long)tlo);
-      atomicXor(t + 1, (unsigned long long)thi);
+    if (io.active) {
+      unsigned long long* t = reinterpret_cast<unsigned long long*>(tags_batch + 16 * io.s);
+      atomicXor(t, (unsigned long long)acc.tlo);
+      atomicXor(t + 1, (unsigned long long)acc.thi);
     }
   } else {
+    uint64_t tlo = acc.tlo, thi = acc.thi;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       tlo ^= __shfl_xor_sync(0xffffffffu, tlo, o);
@@ -630,6 +651,195 @@ __global__ void __launch_bounds__(CTA, (min_ctas<INTEG, CTA>()))
       atomicXor(t + 1, (unsigned long long)thi);
     }
   }
+}
+
+// RN(p / 10^{3+e}) for e = Omega_3 in [0,6) and p a byte, once per CTA (Step 2, Q19)
+template <int CTA>
+__device__ __forceinline__ void fill_theta(double* theta_tab) {
+  for (uint32_t i = threadIdx.x; i < 6 * 256; i += CTA)
+    theta_tab[i] = __ddiv_rn(__uint2double_rn(i & 255), pow10_theta(3 + (i >> 8)));
+}
+
+// ------------------------------------------------------------------ the wave kernel
+// OP: OP_ENC / OP_DEC / OP_VERIFY; CTA: 128, 256 or 512 threads. One lane per block, one
+// warp per 32 consecutive blocks; warps are independent (only __syncwarp), so the CTA never
+// waits on its slowest warp.
+template <int OP, int INTEG, int CTA>
+__global__ void __launch_bounds__(CTA, (min_ctas<INTEG, CTA>()))
+    lorenz_chain_kernel(const DevConst C, const DevKey K1, const DevKey* __restrict__ Kb,
+                        const uint8_t* __restrict__ in, uint8_t* __restrict__ out,
+                        lorenz_result* __restrict__ res, uint8_t* __restrict__ tags_batch,
+                        uint8_t* __restrict__ block_ok) {
+  constexpr int WIN = CTA >= 512 ? 32 : kWin;  // 512-thread CTAs: shorter windows keep smem < 48 KB
+  __shared__ __align__(16) uint8_t stage[(CTA / 32) * 32 * (WIN + 16)];
+  __shared__ double theta_tab[6 * 256];
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  fill_theta<CTA>(theta_tab);
+  __syncthreads();  // the only CTA-wide barrier; warps run independently afterwards
+
+  const LaneIO io = lane_io<OP>(C, in, out, (uint64_t)blockIdx.x * CTA + threadIdx.x);
+  Chain ch;
+  if (io.active) key_schedule(C.batch ? Kb[io.s] : K1, C.fast != 0, (uint32_t)io.bl, C.variant, ch);
+  LaneAcc acc{0, 0, true, false};
+  run_chars<OP, INTEG, WIN>(C, io, ch, acc, stage + warp * 32 * (WIN + 16), theta_tab, 0,
+                            warp_max_u64(io.total), lane);
+  finish_lanes<OP>(C, io, acc, res, tags_batch, block_ok, lane);
+}
+
+// ------------------------------------------------------------------ the balanced kernel
+// The wave kernel gives every SM sub-partition whole warps of 32 chains; when the warp count
+// is not a multiple of the resident slots (C3: 2,048 warps over 592 sub-partitions = 3.46)
+// the sub-partitions holding one warp more finish last and the FP64 pipe idles in the tail
+// (C3: 84.9 % of peak). Here the same work is cut into equal slices instead (McNaughton's
+// wrap-around rule for preemptive scheduling): unit u = 32 consecutive chains of Q 16-char
+// chunks occupies chunk positions [uQ, (u+1)Q) of a line of U*Q, and resident warp slot k
+// takes positions [k Cq, (k+1) Cq), Cq = ceil(U Q / S) >= Q. A unit cut by a slot boundary
+// runs its FIRST chunks at the start of slot k+1, hands its 32 chain states over through
+// global memory, and slot k finishes it at its end; since Q <= Cq the two pieces never
+// overlap in time. Slots are numbered by start order (a ticket), later starters taking
+// earlier positions, so a warp only ever waits on a piece that a warp which started before
+// it runs first thing: no deadlock even when not every CTA is resident.
+struct SegPlan {
+  uint64_t units;  // U = ceil(lanes / 32)
+  uint64_t cq;     // chunks per slot
+  uint32_t q;      // chunks per unit = ceil((B + 16) / 16)
+  uint32_t slots;  // S (<= U)
+};
+constexpr int kSegWords = 18;  // u64 words of one lane's handed-over state
+
+__device__ __forceinline__ void seg_save(uint64_t* dst, uint32_t lane, const Chain& c, const LaneAcc& a) {
+  const uint64_t w[kSegWords] = {
+      (uint64_t)__double_as_longlong(c.x),   (uint64_t)__double_as_longlong(c.y),
+      (uint64_t)__double_as_longlong(c.z),   (uint64_t)__double_as_longlong(c.apx),
+      (uint64_t)__double_as_longlong(c.apy), (uint64_t)__double_as_longlong(c.apz),
+      c.m1, c.m2, c.m3,
+      c.mu1 | ((uint64_t)c.mu2 << 32), c.mu3 | ((uint64_t)c.om1 << 32), c.om2 | ((uint64_t)c.om3 << 32),
+      c.k1 | ((uint64_t)c.k2 << 32),   c.k3 | ((uint64_t)c.ik1 << 32),  c.ik2 | ((uint64_t)c.ik3 << 32),
+      a.tlo, a.thi, (uint64_t)a.guard_ok | ((uint64_t)a.bad << 32)};
+#pragma unroll
+  for (int f = 0; f < kSegWords; ++f) __stcg(dst + f * 32 + lane, w[f]);
+}
+
+__device__ __forceinline__ void seg_load(const uint64_t* src, uint32_t lane, Chain& c, LaneAcc& a) {
+  uint64_t w[kSegWords];
+#pragma unroll
+  for (int f = 0; f < kSegWords; ++f) w[f] = __ldcg(src + f * 32 + lane);
+  c.x = __longlong_as_double((long long)w[0]);
+  c.y = __longlong_as_double((long long)w[1]);
+  c.z = __longlong_as_double((long long)w[2]);
+  c.apx = __longlong_as_double((long long)w[3]);
+  c.apy = __longlong_as_double((long long)w[4]);
+  c.apz = __longlong_as_double((long long)w[5]);
+  c.m1 = w[6]; c.m2 = w[7]; c.m3 = w[8];
+  c.mu1 = (uint32_t)w[9];  c.mu2 = (uint32_t)(w[9] >> 32);
+  c.mu3 = (uint32_t)w[10]; c.om1 = (uint32_t)(w[10] >> 32);
+  c.om2 = (uint32_t)w[11]; c.om3 = (uint32_t)(w[11] >> 32);
+  c.k1 = (uint32_t)w[12];  c.k2 = (uint32_t)(w[12] >> 32);
+  c.k3 = (uint32_t)w[13];  c.ik1 = (uint32_t)(w[13] >> 32);
+  c.ik2 = (uint32_t)w[14]; c.ik3 = (uint32_t)(w[14] >> 32);
+  a.tlo = w[15]; a.thi = w[16];
+  a.guard_ok = (uint32_t)w[17] != 0;
+  a.bad = (uint32_t)(w[17] >> 32) != 0;
+}
+
+__device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+#ifdef LZ_SEG_TRACE  // tuning builds only (tools/seg_trace.py): per-slot timeline
+__device__ unsigned long long g_seg_trace[4096 * 8];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define SEG_TRACE(k, f, v) \
+  do { if (lane == 0 && (k) < 4096) g_seg_trace[(k) * 8 + (f)] = (v); } while (0)
+#else
+#define SEG_TRACE(k, f, v) do {} while (0)
+#endif
+
+// Scratch (zeroed by the host before the launch): seg_ticket[0] = start-order counter,
+// seg_flag[S + 1] = "the first piece of the unit cut at boundary k is done",
+// seg_state[(S + 1) * kSegWords * 32] = the handed-over lane states.
+template <int OP, int INTEG, int CTA>
+__global__ void __launch_bounds__(CTA, 1)
+    lorenz_chain_seg_kernel(const DevConst C, const DevKey K1, const DevKey* __restrict__ Kb,
+                            const uint8_t* __restrict__ in, uint8_t* __restrict__ out,
+                            lorenz_result* __restrict__ res, uint8_t* __restrict__ tags_batch,
+                            uint8_t* __restrict__ block_ok, const SegPlan P, uint32_t* __restrict__ seg_ticket,
+                            uint32_t* __restrict__ seg_flag, uint64_t* __restrict__ seg_state) {
+  constexpr int WIN = CTA >= 512 ? 32 : kWin;  // 512-thread CTAs: shorter windows keep smem < 48 KB
+  __shared__ __align__(16) uint8_t stage[(CTA / 32) * 32 * (WIN + 16)];
+  __shared__ double theta_tab[6 * 256];
+  __shared__ uint32_t s_ticket;
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  fill_theta<CTA>(theta_tab);
+  if (threadIdx.x == 0) s_ticket = atomicAdd(seg_ticket, 1u);
+  __syncthreads();
+  const uint64_t t = (uint64_t)s_ticket * (CTA / 32) + warp;  // start order
+  if (t >= P.slots) return;
+  const uint64_t k = P.slots - 1 - t;  // later starters take earlier positions
+  const uint64_t Q = P.q, UQ = P.units * Q;
+  const uint64_t X0 = k * P.cq;
+  if (X0 >= UQ) return;
+  const uint64_t X1 = (X0 + P.cq < UQ) ? X0 + P.cq : UQ;
+  uint8_t* wst = stage + warp * 32 * (WIN + 16);
+  uint64_t u = X0 / Q;
+#ifdef LZ_SEG_TRACE
+  {
+    uint32_t smid, wid;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+    asm volatile("mov.u32 %0, %warpid;" : "=r"(wid));
+    SEG_TRACE(k, 0, gtimer());
+    SEG_TRACE(k, 6, ((unsigned long long)smid << 32) | wid);
+    SEG_TRACE(k, 7, t);
+  }
+#endif
+
+  if (X0 % Q) {  // first piece: chunks [0, a) of unit u, which slot k-1 finishes
+    const uint64_t a = (u + 1) * Q - X0;
+    const LaneIO io = lane_io<OP>(C, in, out, u * 32 + lane);
+    Chain ch;
+    if (io.active) key_schedule(C.batch ? Kb[io.s] : K1, C.fast != 0, (uint32_t)io.bl, C.variant, ch);
+    LaneAcc acc{0, 0, true, false};
+    run_chars<OP, INTEG, WIN, true>(C, io, ch, acc, wst, theta_tab, 0, 16 * a, lane);
+    seg_save(seg_state + k * (kSegWords * 32), lane, ch, acc);
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) st_release_u32(seg_flag + k, 1u);
+    SEG_TRACE(k, 1, gtimer());
+    ++u;
+  }
+  for (; (u + 1) * Q <= X1; ++u) {  // whole units
+    const LaneIO io = lane_io<OP>(C, in, out, u * 32 + lane);
+    Chain ch;
+    if (io.active) key_schedule(C.batch ? Kb[io.s] : K1, C.fast != 0, (uint32_t)io.bl, C.variant, ch);
+    LaneAcc acc{0, 0, true, false};
+    run_chars<OP, INTEG, WIN, true>(C, io, ch, acc, wst, theta_tab, 0, 16 * Q, lane);
+    finish_lanes<OP>(C, io, acc, res, tags_batch, block_ok, lane);
+  }
+  if (u * Q < X1) {  // last piece: chunks [a, Q) of unit u, whose first a chunks open slot k+1
+    const uint64_t a = (u + 1) * Q - X1;
+    const LaneIO io = lane_io<OP>(C, in, out, u * 32 + lane);
+    SEG_TRACE(k, 2, gtimer());
+    if (lane == 0)
+      while (ld_acquire_u32(seg_flag + k + 1) == 0) __nanosleep(256);
+    __syncwarp();
+    SEG_TRACE(k, 3, gtimer());
+    (void)ld_acquire_u32(seg_flag + k + 1);
+    Chain ch;
+    LaneAcc acc;
+    seg_load(seg_state + (k + 1) * (kSegWords * 32), lane, ch, acc);
+    run_chars<OP, INTEG, WIN, true>(C, io, ch, acc, wst, theta_tab, 16 * a, 16 * Q, lane);
+    finish_lanes<OP>(C, io, acc, res, tags_batch, block_ok, lane);
+  }
+  SEG_TRACE(k, 4, gtimer());
 }
 
 // Zero the plaintext slice if the launch found an integrity failure (async decrypt

@@ -30,7 +30,8 @@ EXPORTS = ["lorenz_abi_version", "lorenz_last_error", "lorenz_status_string", "l
            "lorenz_encrypt_batch", "lorenz_encrypt_host", "lorenz_decrypt_host",
            "lorenz_compare_spans", "lorenz_histograms", "lorenz_envelope_write", "lorenz_envelope_read",
            "lorenz_encrypt_file", "lorenz_decrypt_file", "lorenz_digit_histograms",
-           "lorenz_autocorrelation", "lorenz_power_spectrum", "lorenz_encrypt_ragged", "lorenz_decrypt_ragged"]
+           "lorenz_autocorrelation", "lorenz_power_spectrum", "lorenz_encrypt_ragged", "lorenz_decrypt_ragged",
+           "lorenz_launch_plan"]
 E_IO, E_FORMAT = 7, 8
 ENVELOPE_BYTES = 24
 
@@ -89,6 +90,7 @@ def lib():
         L.lorenz_ct_len.argtypes = [kp, u64]
         L.lorenz_ct_len.restype = u64
         L.lorenz_pt_len.argtypes = [kp, u64, C.POINTER(u64)]
+        L.lorenz_launch_plan.argtypes = [kp, u64, u64, u64, C.POINTER(lorenz_plan)]
         L.lorenz_encrypt.argtypes = [kp, u64, u64, u64, vp, vp, vp, vp]
         L.lorenz_decrypt.argtypes = [kp, u64, u64, u64, vp, vp, C.POINTER(C.c_int64), vp, vp]
         L.lorenz_verify.argtypes = [kp, u64, u64, u64, vp, C.POINTER(C.c_int64), vp, vp]
@@ -173,6 +175,20 @@ def lorenz_keysetup(pw: bytes, mode: int = FAST, n_it: int = 0, dt_code: int = 0
     p = lorenz_params(mode, n_it, dt_code, block_size, integrator, variant)
     _check(lib().lorenz_keysetup(bytes(pw), len(pw), C.byref(p), C.byref(k)), "lorenz_keysetup")
     return Key(k)
+
+
+class lorenz_plan(C.Structure):
+    _fields_ = [("kind", C.c_uint32), ("cta", C.c_uint32), ("grid", C.c_uint64), ("lanes", C.c_uint64),
+                ("slots", C.c_uint64), ("chunks_per_slot", C.c_uint64)]
+
+
+def lorenz_launch_plan(key: Key, n: int, b0: int, b1: int) -> dict:
+    """The chain kernel's launch plan for blocks [b0, b1) (host only): kind 'wave' or 'balanced',
+    CTA size, grid, lanes, and for the balanced kernel its warp slots and chunks per slot."""
+    p = lorenz_plan()
+    _check(lib().lorenz_launch_plan(C.byref(key.raw), n, b0, b1, C.byref(p)), "lorenz_launch_plan")
+    return {"kind": ("wave", "balanced")[p.kind], "cta": p.cta, "grid": p.grid, "lanes": p.lanes,
+            "slots": p.slots, "chunks_per_slot": p.chunks_per_slot}
 
 
 def lorenz_num_blocks(key: Key, n: int) -> int:

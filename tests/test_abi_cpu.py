@@ -103,3 +103,33 @@ def test_product_never_imports_oracle():
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt, f
                 assert "lorenz_ref" not in txt, f
+
+
+def test_launch_plan_rules(L, monkeypatch):
+    """Host-side schedule choice, computed without a device (148 SMs): the
+    balanced kernel for 2+ warps per SM sub-partition and under three waves unless the wave
+    kernel's single wave splits evenly; the wave kernel otherwise; overrides honoured."""
+    monkeypatch.delenv("LORENZ_SCHED", raising=False)
+    monkeypatch.delenv("LORENZ_SEG_SLOTS", raising=False)
+    key = L.lorenz_keysetup(b"0123456789abcdef", mode=L.FAST)
+    plan = lambda blocks: L.lorenz_launch_plan(key, blocks * 1024, 0, blocks)
+    p = plan(65536)  # C3: 2,048 units, 3.46 warps per sub-partition in one wave
+    assert p["kind"] == "balanced" and p["cta"] == 384 and p["grid"] == 148 and p["slots"] == 1776
+    assert p["chunks_per_slot"] == -(-2048 * 65 // 1776) >= 65
+    assert plan(131072)["kind"] == "balanced" and plan(131072)["cta"] == 512  # C4 per rank at N = 8
+    assert plan(1 << 20)["kind"] == "wave"           # C4 at N = 1: 13.8 waves
+    assert plan(262144)["kind"] == "wave"            # C4 per rank at N = 4
+    assert plan(75776)["kind"] == "wave"             # exactly 4 warps per sub-partition
+    assert plan(37888)["kind"] == "wave"             # exactly 2 warps per sub-partition
+    assert plan(1024)["kind"] == "wave" and plan(1024)["grid"] * plan(1024)["cta"] >= 1024  # C2
+    assert L.lorenz_launch_plan(key, 0, 0, 1)["lanes"] == 1
+    fma = L.lorenz_keysetup(b"0123456789abcdef", mode=L.FAST, integrator=L.RK4_FMA)
+    assert L.lorenz_launch_plan(fma, 65536 * 1024, 0, 65536)["kind"] == "wave"
+    monkeypatch.setenv("LORENZ_SCHED", "wave")
+    assert plan(65536)["kind"] == "wave"
+    monkeypatch.setenv("LORENZ_SCHED", "seg")
+    monkeypatch.setenv("LORENZ_SEG_SLOTS", "3")
+    p = plan(160)
+    assert p["kind"] == "balanced" and p["slots"] == 3 and p["chunks_per_slot"] == 109
+    with pytest.raises(L.LorenzError):
+        L.lorenz_launch_plan(key, 1024, 0, 2)

@@ -1,0 +1,219 @@
+"""GPU parity of the balanced (McNaughton) schedule of the chain kernel.
+
+`lorenz_chain_seg_kernel` cuts the launch's 32-chain units at slot boundaries and hands the
+32 chain states of a cut unit from one warp to another through global memory.
+The library picks it for launches with >= 2 warps of chains per SM sub-partition; here
+LORENZ_SEG_SLOTS forces small slot counts so that small messages — ones the oracle checks
+byte for byte — are cut at many places: unit boundaries, mid-window, the sentinel, a ragged
+last block. Integer outputs, tolerance 0, against the oracle and against the wave kernel.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_1201_3114_b200 import inputs
+from paper_1201_3114_b200 import lorenz as L
+
+pytestmark = pytest.mark.gpu
+DEV = torch.device("cuda:0")
+
+
+@pytest.fixture
+def sched(monkeypatch):
+    """Set the schedule overrides for this test (the library reads them at every launch)."""
+    def set_(slots=None, mode=None):
+        if slots is None:
+            monkeypatch.delenv("LORENZ_SEG_SLOTS", raising=False)
+        else:
+            monkeypatch.setenv("LORENZ_SEG_SLOTS", str(slots))
+        if mode is None:
+            monkeypatch.delenv("LORENZ_SCHED", raising=False)
+        else:
+            monkeypatch.setenv("LORENZ_SCHED", mode)
+    yield set_
+    set_()
+
+
+def oparams(key):
+    p = key.params
+    return oracle.params(mode=p.mode, n_it=p.n_it, dt_code=p.dt_code, block_size=p.block_size,
+                         integrator=p.integrator, variant=p.variant)
+
+
+def run_all(key, msg):
+    n = len(msg)
+    nb = key.num_blocks(n)
+    pt = torch.from_numpy(msg).to(DEV)
+    ct = torch.zeros(key.ct_len(n), dtype=torch.uint8, device=DEV)
+    tag = L.lorenz_encrypt(key, n, 0, nb, pt, ct)
+    return ct, tag
+
+
+# (blocks, trailing bytes of a ragged last block, slots): units = ceil(blocks / 32)
+CASES = [(160, 0, 3), (160, 0, 4), (161, 300, 3), (200, 1, 5), (257, 1023, 7), (96, 0, 2), (64, 17, 2),
+         (33, 0, 2), (300, 512, 9)]
+
+
+@pytest.mark.parametrize("blocks,tail,slots", CASES)
+@pytest.mark.parametrize("integrator", [L.RK4, L.EULER])
+def test_seg_matches_oracle(sched, blocks, tail, slots, integrator):
+    sched(slots=slots)
+    n = (blocks - (1 if tail else 0)) * 1024 + tail
+    pw = inputs.password(seed=blocks * 31 + slots)
+    msg = inputs.message(n, seed=blocks + tail)
+    key = L.lorenz_keysetup(pw, mode=L.FAST, n_it=7, integrator=integrator)
+    ct, tag = run_all(key, msg)
+    want, want_tag = oracle.encrypt(pw, msg, oparams(key))
+    got = ct.cpu().numpy()
+    if not np.array_equal(got, want):
+        bad = np.nonzero(got != want)[0]
+        raise AssertionError(f"{len(bad)} bytes differ, first at {bad[0]} (block {bad[0] // 1040})")
+    assert tag == want_tag
+    nb = key.num_blocks(n)
+    st, fb, vtag = L.lorenz_verify(key, n, 0, nb, ct)
+    assert (st, fb, vtag) == (L.OK, -1, tag)
+    back = torch.empty(n, dtype=torch.uint8, device=DEV)
+    ok = torch.zeros(nb, dtype=torch.uint8, device=DEV)
+    st, fb = L.lorenz_decrypt(key, n, 0, nb, ct, back, block_ok=ok)
+    assert (st, fb) == (L.OK, -1)
+    assert np.array_equal(back.cpu().numpy(), msg)
+    assert bool((ok == 1).all())
+
+
+def test_seg_tamper_in_every_piece(sched):
+    """Flips in the first piece, the second piece and the tag of cut units (and in a whole unit)
+    are reported with the right block; every other block decrypts intact."""
+    sched(slots=3)
+    blocks = 160  # 5 units of 65 chunks over 3 slots: cuts at chunks 109 and 218
+    n = blocks * 1024
+    pw = inputs.password(seed=5)
+    msg = inputs.message(n, seed=5)
+    key = L.lorenz_keysetup(pw, mode=L.FAST, n_it=7)
+    ct, _ = run_all(key, msg)
+    clean = ct.clone()
+    prm = oparams(key)
+    # unit 1 (blocks 32..63) is cut at chunk 109 - 65 = 44 (char 704); unit 3 at chunk 218 - 195 = 23
+    for blk, off in [(40, 100), (40, 900), (40, 1030), (100, 300), (100, 1039), (5, 512), (159, 1)]:
+        ct.copy_(clean)
+        pos = blk * 1040 + off
+        ct[pos] ^= 0x40
+        st, fb, _ = L.lorenz_verify(key, n, 0, blocks, ct)
+        assert (st, fb) == (L.E_INTEGRITY, blk)
+        back = torch.full((n,), 7, dtype=torch.uint8, device=DEV)
+        ok = torch.zeros(blocks, dtype=torch.uint8, device=DEV)
+        st, fb = L.lorenz_decrypt(key, n, 0, blocks, ct, back, block_ok=ok)
+        assert (st, fb) == (L.E_INTEGRITY, blk)
+        okh = ok.cpu().numpy()
+        assert okh[blk] == 0 and okh.sum() == blocks - 1
+        got = back.cpu().numpy()
+        assert not got[blk * 1024:(blk + 1) * 1024].any()
+        mask = np.ones(n, dtype=bool)
+        mask[blk * 1024:(blk + 1) * 1024] = False
+        assert np.array_equal(got[mask], msg[mask])
+        ost, _, ofb, ook = oracle.decrypt(pw, ct.cpu().numpy(), prm, per_block=True)
+        assert ofb == blk and np.array_equal(ook, okh)
+
+
+@pytest.mark.parametrize("slots", [2, 3, 11])
+def test_seg_block_range_slice(sched, slots):
+    """A rank's slice [b0, b1) of a larger message through the cut schedule."""
+    sched(slots=slots)
+    n = 400 * 1024 + 77
+    pw = inputs.password(seed=9)
+    msg = inputs.message(n, seed=9)
+    key = L.lorenz_keysetup(pw, mode=L.FAST, n_it=5)
+    b0, b1 = 37, 401
+    pt = torch.from_numpy(msg[b0 * 1024:]).to(DEV)
+    ct = torch.zeros(key.ct_len(n) - b0 * 1040, dtype=torch.uint8, device=DEV)
+    tag = L.lorenz_encrypt(key, n, b0, b1, pt, ct)
+    want, want_tag = oracle.encrypt(pw, msg, oparams(key), b0=b0, b1=b1)
+    assert np.array_equal(ct.cpu().numpy(), want[b0 * 1040:])
+    assert tag == want_tag
+
+
+@pytest.mark.parametrize("variant", [1, 2, 4, 5])
+def test_seg_step3_variants(sched, variant):
+    sched(slots=4)
+    n = 190 * 1024 + 5
+    pw = inputs.password(seed=variant)
+    msg = inputs.message(n, seed=variant)
+    key = L.lorenz_keysetup(pw, mode=L.FAST, n_it=6, variant=variant)
+    ct, tag = run_all(key, msg)
+    want, want_tag = oracle.encrypt(pw, msg, oparams(key))
+    assert np.array_equal(ct.cpu().numpy(), want) and tag == want_tag
+
+
+def test_seg_batch_and_ragged(sched):
+    """lorenz_encrypt_batch (C5 shape) and ragged batches through the cut schedule."""
+    sched(slots=5)
+    S, n = 6, 50 * 1024 + 48  # the batch call needs n % 16 == 0
+    pws = [inputs.password(seed=100 + s) for s in range(S)]
+    keys = [L.lorenz_keysetup(pw, mode=L.FAST, n_it=5) for pw in pws]
+    msgs = [inputs.message(n, seed=200 + s) for s in range(S)]
+    pts = torch.from_numpy(np.concatenate(msgs)).to(DEV)
+    cl = keys[0].ct_len(n)
+    cts = torch.zeros(S * cl, dtype=torch.uint8, device=DEV)
+    tags = torch.zeros(16 * S, dtype=torch.uint8, device=DEV)
+    L.lorenz_encrypt_batch(keys, n, pts, cts, tags)
+    prm = oparams(keys[0])
+    for s in range(S):
+        want, want_tag = oracle.encrypt(pws[s], msgs[s], prm)
+        assert np.array_equal(cts[s * cl:(s + 1) * cl].cpu().numpy(), want)
+        assert tags[16 * s:16 * s + 16].cpu().numpy().tobytes() == want_tag
+
+    lengths = [33 * 1024, 5, 0, 70 * 1024 + 100, 1024, 40 * 1024 - 1]
+    up = lambda x: (x + 15) // 16 * 16
+    pt_off, ct_off, p, c = [], [], 0, 0
+    for m in lengths:
+        pt_off.append(p)
+        ct_off.append(c)
+        p += up(m)
+        c += up(keys[0].ct_len(m))
+    host = np.zeros(p, dtype=np.uint8)
+    rmsgs = []
+    for s, m in enumerate(lengths):
+        rmsgs.append(inputs.message(m, seed=300 + s))
+        host[pt_off[s]:pt_off[s] + m] = rmsgs[-1]
+    rpts = torch.from_numpy(host).to(DEV)
+    rcts = torch.zeros(c, dtype=torch.uint8, device=DEV)
+    rtags = torch.zeros(16 * len(lengths), dtype=torch.uint8, device=DEV)
+    L.lorenz_encrypt_ragged(keys, lengths, pt_off, ct_off, rpts, rcts, rtags)
+    rh = rcts.cpu().numpy()
+    for s, m in enumerate(lengths):
+        want, want_tag = oracle.encrypt(pws[s], rmsgs[s], prm)
+        assert np.array_equal(rh[ct_off[s]:ct_off[s] + len(want)], want), f"message {s}"
+        assert rtags[16 * s:16 * s + 16].cpu().numpy().tobytes() == want_tag
+    back = torch.zeros_like(rpts)
+    st, fb = L.lorenz_decrypt_ragged(keys, lengths, ct_off, pt_off, rcts, back, torch.empty_like(rtags))
+    assert st == L.OK and fb == [-1] * len(lengths)
+    assert torch.equal(back, rpts)
+
+
+@pytest.mark.parametrize("mib", [64, 150])
+def test_seg_default_equals_wave(sched, mib):
+    """At sizes where the library picks the cut schedule by itself (C3: 2,048 units over 1,184
+    slots; 150 MiB: 4,800 units over 2,368), its ciphertext, tag and verdicts equal the wave
+    kernel's, and sampled blocks equal the oracle's."""
+    n = mib << 20
+    pw = inputs.password()
+    msg = inputs.message(n, seed=mib)
+    key = L.lorenz_keysetup(pw, mode=L.FAST)
+    pt = torch.from_numpy(msg).to(DEV)
+    nb = key.num_blocks(n)
+    sched()
+    ct_seg = torch.empty(key.ct_len(n), dtype=torch.uint8, device=DEV)
+    tag_seg = L.lorenz_encrypt(key, n, 0, nb, pt, ct_seg)
+    sched(mode="wave")
+    ct_wave = torch.empty_like(ct_seg)
+    tag_wave = L.lorenz_encrypt(key, n, 0, nb, pt, ct_wave)
+    assert tag_seg == tag_wave
+    assert torch.equal(ct_seg, ct_wave)
+    sched()
+    st, fb, vtag = L.lorenz_verify(key, n, 0, nb, ct_seg)
+    assert (st, fb, vtag) == (L.OK, -1, tag_seg)
+    prm = oparams(key)
+    rng = np.random.default_rng(mib)
+    for b in [0, nb - 1] + [int(x) for x in rng.integers(0, nb, 6)]:
+        want = oracle.encrypt_block(pw, n, b, msg[b * 1024:(b + 1) * 1024], prm)
+        assert np.array_equal(ct_seg[b * 1040:(b + 1) * 1040].cpu().numpy(), want), f"block {b}"

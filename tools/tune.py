@@ -23,6 +23,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--tag", default=os.environ.get("LORENZ_LIB", "default"))
     ap.add_argument("--mib", type=int, nargs="+", default=[64, 128, 256, 1024])
+    ap.add_argument("--kib", type=int, nargs="+", default=None, help="sizes in KiB (= blocks at B = 1024)")
     ap.add_argument("--n-it", type=int, default=100)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--integrator", choices=["rk4", "euler", "rk4fma"], default="rk4")
@@ -30,13 +31,13 @@ def main():
     dev = torch.device("cuda:0")
     integ = {"rk4": L.RK4, "euler": L.EULER, "rk4fma": L.RK4_FMA}[a.integrator]
     key = L.lorenz_keysetup(inputs.password(), mode=L.FAST, n_it=a.n_it, integrator=integ)
-    big = max(a.mib) << 20
+    sizes = [k << 10 for k in a.kib] if a.kib else [m << 20 for m in a.mib]
+    big = max(sizes)
     msg = torch.from_numpy(inputs.message(big)).to(dev)
     ct = torch.empty(key.ct_len(big), dtype=torch.uint8, device=dev)
     res = torch.empty(32, dtype=torch.uint8, device=dev)
     peak = 148 * 64 * 1965e6
-    for mib in a.mib:
-        n = mib << 20
+    for n in sizes:
         nb = key.num_blocks(n)
         L.lorenz_result_init_async(res)
         L.lorenz_encrypt_async(key, n, 0, nb, msg, ct, res)
@@ -51,7 +52,7 @@ def main():
             ts.append(e0.elapsed_time(e1) / 1e3)
         t = min(ts)
         ops = fp64_ops(n, 1024, 0, nb, a.n_it, a.integrator)
-        print(json.dumps({"tag": a.tag, "integrator": a.integrator, "mib": mib, "blocks": nb, "ms": round(t * 1e3, 3),
+        print(json.dumps({"tag": a.tag, "integrator": a.integrator, "mib": round(n / 2**20, 3), "blocks": nb, "ms": round(t * 1e3, 3),
                           "MBps": round(n / t / 1e6, 1), "frac": round(ops / t / peak, 4)}), flush=True)
 
 
