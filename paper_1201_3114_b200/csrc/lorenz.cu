@@ -1064,8 +1064,8 @@ constexpr uint64_t kHostChunk = 128ull << 20;  // upper bound of an automatic ho
 }  // namespace
 
 // Blocks [B0,B1) from host slices: chunked H2D -> kernel -> D2H over HostPipe's streams.
-// Blocks [B0,B1) from host slices. The slice is cut into block-aligned chunks (default: at least
-// 8, at most ~128 MiB each); chunk c runs on slot c % S (S = min(8, chunks)), each slot owning a
+// The slice is cut into block-aligned chunks (default: at most ~128 MiB each, and up to 8
+// while each chunk still fills the SMs); chunk c runs on slot c % S (S = min(8, chunks)), each slot owning a
 // stream and device buffers sized for one chunk. Chunk c + S reuses the slot's buffers only
 // after chunk c's D2H (same stream), so the host never waits and device memory stays bounded
 // (≈ 8 x 2 x 128 MiB) whatever the message size: messages larger than HBM work.
@@ -1080,7 +1080,13 @@ static lorenz_status host_range(const lorenz_key* k, uint64_t n, uint64_t B0, ui
   lorenz_status ret = check_range(K, n, B0, B1, in_host, inb, out_host, outb);
   if (ret != LORENZ_OK || B0 == B1) return ret;
   const uint64_t nbk = B1 - B0;
-  uint64_t C = n_chunks ? n_chunks : std::max<uint64_t>(8, (inb + kHostChunk - 1) / kHostChunk);
+  // automatic: chunks of at most kHostChunk, and up to 8 (for copy/compute overlap) as long as
+  // each keeps >= 2 warps of chains per SM sub-partition, the least a launch needs to keep the
+  // FP64 pipe busy (C3, 64 MiB: one chunk; 8 chunks of 8 MiB ran at 82 % of the device rate)
+  const uint64_t units = (nbk + 31) / 32, per = 8 * (uint64_t)sm_count();
+  uint64_t C = n_chunks ? n_chunks
+                        : std::max<uint64_t>((inb + kHostChunk - 1) / kHostChunk,
+                                             std::min<uint64_t>(8, std::max<uint64_t>(1, units / per)));
   if (C > nbk) C = nbk;
   const uint32_t S = (uint32_t)std::min<uint64_t>(C, HostPipe::kStreams);
   const uint64_t Bsz = block_B(K, n);
