@@ -335,9 +335,12 @@ void set_last_error(const std::string& s) { g_err = s; }  // shared with lorenz_
 extern "C" {
 
 #ifdef LZ_SEG_TRACE
-// Tuning builds only: copy the last balanced launch's per-slot timeline (4096 x 8 u64).
+// Tuning builds only: copy the per-slot timeline (4096 x 8 u64) out, then zero it (slots with no
+// work record nothing, so rows of an earlier launch would otherwise survive).
 int lorenz_debug_seg_trace(unsigned long long* host) {
-  return cudaMemcpyFromSymbol(host, lz::g_seg_trace, sizeof lz::g_seg_trace) == cudaSuccess ? 0 : 1;
+  if (cudaMemcpyFromSymbol(host, lz::g_seg_trace, sizeof lz::g_seg_trace) != cudaSuccess) return 1;
+  static unsigned long long zeros[4096 * 8];
+  return cudaMemcpyToSymbol(lz::g_seg_trace, zeros, sizeof zeros) == cudaSuccess ? 0 : 1;
 }
 #endif
 

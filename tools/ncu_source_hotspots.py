@@ -2,6 +2,7 @@
 --import-source on at capture time).
 
 Usage: python tools/ncu_source_hotspots.py gpurun_out/prof.ncu-rep [--top 15] [--json out.json]
+       (or the `ncu -i REP --page source --csv --print-source sass,cuda` export, .csv or .csv.gz)
 Reports each source line's share of all stall samples, and the share on the RK4 loop body
 (the lines of integrate<>, identified by their k1..k4 / a,b,c / s-update statements).
 """
@@ -24,8 +25,12 @@ def main():
     ap.add_argument("--top", type=int, default=15)
     ap.add_argument("--json")
     a = ap.parse_args()
-    txt = subprocess.run(["ncu", "-i", a.rep, "--page", "source", "--csv", "--print-source", "sass,cuda"],
-                         capture_output=True, text=True).stdout
+    if a.rep.endswith((".csv", ".csv.gz")):  # the source page exported on the box (rep too big to ship)
+        import gzip
+        txt = (gzip.open if a.rep.endswith(".gz") else open)(a.rep, "rt").read()
+    else:
+        txt = subprocess.run(["ncu", "-i", a.rep, "--page", "source", "--csv", "--print-source", "sass,cuda"],
+                             capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(txt)))
     out, file = [], ""
     samp_i = None

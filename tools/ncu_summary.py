@@ -3,6 +3,7 @@ one `--set full` capture of the chain kernel (FP64 pipe, DRAM traffic, occupancy
 
 Usage: python tools/ncu_summary.py --launches gpurun_out/launches.csv --rep gpurun_out/prof.ncu-rep \
            --out profiles/ncu_chain_kernel.json [--world 1]
+       (--rep also takes the `--page raw --csv` export of a report, for reports too big to ship back)
 """
 import argparse
 import collections
@@ -50,7 +51,10 @@ def launches(path):
 
 
 def full(rep):
-    txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if rep.endswith(".csv"):  # `ncu -i REP --page raw --csv` exported on the box
+        txt = open(rep).read()
+    else:
+        txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(txt)))
     h, units = rows[0], rows[1]
     out = []

@@ -45,7 +45,7 @@ def main():
         L.lorenz_encrypt_async(key, n, 0, nb, msg, ct, res)  # warm
         torch.cuda.synchronize()
         tr = np.zeros(4096 * 8, dtype=np.uint64)
-        lib.lorenz_debug_seg_trace(tr.ctypes.data)  # clear stale rows by reading after a fresh launch
+        lib.lorenz_debug_seg_trace(tr.ctypes.data)  # read-and-clear: drop the warm-up launch's rows
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         L.lorenz_encrypt_async(key, n, 0, nb, msg, ct, res)
