@@ -222,7 +222,8 @@ def test_async_api_and_result_slot():
 
 
 def test_async_calls_capture_into_a_cuda_graph():
-    """The _async calls enqueue only kernels (no allocation, no sync): a whole
+    """The _async calls enqueue only stream-ordered work (kernels; the balanced kernel adds a pool
+    allocation and a memset), no synchronisation: a whole
     init -> encrypt -> init -> decrypt sequence is captured once and replayed."""
     pw = inputs.password()
     n = 6 * 1024 + 3

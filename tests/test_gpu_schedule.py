@@ -217,3 +217,91 @@ def test_seg_default_equals_wave(sched, mib):
     for b in [0, nb - 1] + [int(x) for x in rng.integers(0, nb, 6)]:
         want = oracle.encrypt_block(pw, n, b, msg[b * 1024:(b + 1) * 1024], prm)
         assert np.array_equal(ct_seg[b * 1040:(b + 1) * 1040].cpu().numpy(), want), f"block {b}"
+
+
+def test_seg_async_calls_capture_into_a_cuda_graph(sched):
+    """The balanced launch (scratch from the stream-ordered pool, a memset, the kernel, the free)
+    captures into a CUDA graph; replays re-zero the ticket and flags and stay bit-exact."""
+    sched(slots=5, mode="seg")
+    pw = inputs.password(seed=17)
+    n = 200 * 1024 + 3
+    msg = inputs.message(n, seed=17)
+    key = L.lorenz_keysetup(pw, mode=L.FAST, n_it=5)
+    nb = key.num_blocks(n)
+    assert L.lorenz_launch_plan(key, n, 0, nb)["kind"] == "balanced"
+    pt = torch.from_numpy(msg).to(DEV)
+    ct = torch.empty(key.ct_len(n), dtype=torch.uint8, device=DEV)
+    back = torch.empty(n, dtype=torch.uint8, device=DEV)
+    res = torch.empty(64, dtype=torch.uint8, device=DEV)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        L.lorenz_result_init_async(res[:32], stream=s)
+        L.lorenz_encrypt_async(key, n, 0, nb, pt, ct, res[:32], stream=s)
+        L.lorenz_result_init_async(res[32:], stream=s)
+        L.lorenz_decrypt_async(key, n, 0, nb, ct, back, res[32:], stream=s)
+    want, want_tag = oracle.encrypt(pw, msg, oparams(key))
+    for _ in range(3):
+        ct.zero_()
+        back.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        assert np.array_equal(ct.cpu().numpy(), want)
+        r = res.cpu().numpy()
+        assert r[:16].tobytes() == want_tag
+        assert int(r[48:56].view(np.uint64)[0]) == 2 ** 64 - 1
+        assert torch.equal(back, pt)
+
+
+@pytest.mark.timeout(300)
+def test_seg_concurrent_launches_with_a_full_gpu_kernel(sched):
+    """Balanced launches from several host threads on their own streams while a long wave
+    kernel holds every SM: CTAs of one balanced launch start at different times and some wait
+    for SM space, but a warp only waits on slots that started before it (start-order tickets),
+    so every launch completes, bit-exact."""
+    import threading
+    sched(slots=37, mode="seg")
+    big_n = 37888 * 1024  # exactly 2 warps per SM sub-partition: the library's wave kernel
+    big_key = L.lorenz_keysetup(inputs.password(seed=1), mode=L.FAST, n_it=100)
+    big_pt = torch.from_numpy(inputs.message(big_n, seed=1)).to(DEV)
+    big_ct = torch.empty(big_key.ct_len(big_n), dtype=torch.uint8, device=DEV)
+    cases = []
+    for t in range(4):
+        pw = inputs.password(seed=300 + t)
+        n = 50 * 32 * 1024 - 77 * t  # 50 units over 37 slots
+        cases.append((pw, L.lorenz_keysetup(pw, mode=L.FAST, n_it=9), inputs.message(n, seed=400 + t)))
+    out, errors = [None] * len(cases), []
+
+    def work(i):
+        try:
+            pw, key, msg = cases[i]
+            n = len(msg)
+            st = torch.cuda.Stream(device=DEV)
+            with torch.cuda.stream(st):
+                pt = torch.from_numpy(msg).to(DEV)
+                ct = torch.empty(key.ct_len(n), dtype=torch.uint8, device=DEV)
+                tag = L.lorenz_encrypt(key, n, 0, key.num_blocks(n), pt, ct, stream=st)
+                out[i] = (ct.cpu().numpy(), tag)
+        except Exception as e:
+            errors.append(f"thread {i}: {e!r}")
+
+    bs = torch.cuda.Stream(device=DEV)
+    sched(mode="wave")  # the long kernel: every SM busy for ~16 ms
+    big_plan = L.lorenz_launch_plan(big_key, big_n, 0, big_key.num_blocks(big_n))
+    with torch.cuda.stream(bs):
+        res = torch.empty(32, dtype=torch.uint8, device=DEV)
+        L.lorenz_result_init_async(res, stream=bs)
+        L.lorenz_encrypt_async(big_key, big_n, 0, big_key.num_blocks(big_n), big_pt, big_ct, res, stream=bs)
+    sched(slots=37, mode="seg")
+    threads = [threading.Thread(target=work, args=(i,)) for i in range(len(cases))]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    bs.synchronize()
+    assert not errors, errors
+    assert big_plan["kind"] == "wave" and big_plan["grid"] * big_plan["cta"] >= 37888
+    for (pw, key, msg), (ct, tag) in zip(cases, out):
+        want, want_tag = oracle.encrypt(pw, msg, oparams(key))
+        assert np.array_equal(ct, want) and tag == want_tag
