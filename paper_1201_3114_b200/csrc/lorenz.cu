@@ -176,7 +176,7 @@ cudaError_t launch_chain_cta(const lz::DevConst& C, const lz::DevKey& K, const l
 
 void keep_pool_cached();
 
-// Balanced schedule (lz::lorenz_chain_seg_kernel, lorenz_device.cuh) for RK4 / Euler launches
+// Balanced schedule (lz::lorenz_chain_seg_kernel, lorenz_device.cuh) for chain launches
 // with two or more warps of chains per SM sub-partition and fewer than three waves (rules
 // below): one CTA of 128 w threads per SM,
 // S = SMs x 4 x w warp slots, w = min(4, warps per sub-partition) (tools/tune.py: 2 warps per
@@ -186,7 +186,7 @@ void keep_pool_cached();
 // slots cut across the two classes waited), while the warps of one CTA keep within ~3 %.
 // Overrides for tests and tuning: LORENZ_SCHED=wave|seg, LORENZ_SEG_SLOTS=S (clamped to U).
 bool seg_plan(const lz::DevConst& C, uint32_t integrator, lz::SegPlan* P, int* cta) {
-  if (integrator != LORENZ_RK4 && integrator != LORENZ_EULER) return false;
+  if (integrator > LORENZ_RK4_FMA) return false;
   const char* sched = std::getenv("LORENZ_SCHED");
   if (sched && std::strcmp(sched, "wave") == 0) return false;
   const uint64_t U = (C.lanes + 31) / 32, sms = (uint64_t)sm_count();
@@ -198,6 +198,10 @@ bool seg_plan(const lz::DevConst& C, uint32_t integrator, lz::SegPlan* P, int* c
     // against 97.0-97.2 % here), and in one wave whose warps split evenly over the SM
     // sub-partitions (2 per sub-partition per 256-thread CTA).
     if (w < 2 || U > 3 * 16 * sms) return false;
+    // RK4-FMA: the wave kernel runs 20 warps per SM (5 x 128 threads, <= 102 registers), which
+    // its shorter dependent chains need; the balanced kernel's 12-16 reach ~85 %, so it only wins
+    // while the wave kernel's single wave splits badly (C3: 85 % vs 78 %; 128 MiB: 84 % vs 90 %)
+    if (integrator == LORENZ_RK4_FMA && U >= 24 * sms) return false;
     if (U <= 16 * sms) {
       const uint64_t per_smsp_max = 2 * ((((U + 7) / 8) + sms - 1) / sms);
       if (100 * U >= 99 * 4 * sms * per_smsp_max) return false;
@@ -258,6 +262,8 @@ cudaError_t launch_chain(const lz::DevConst& C, const lz::DevKey& K, const lz::D
   if (seg_plan(C, integrator, &P, &scta))
     return integrator == LORENZ_EULER
                ? launch_seg_cta<OP, LORENZ_EULER>(C, P, scta, K, Kb, in, out, res, tags, block_ok, st)
+           : integrator == LORENZ_RK4_FMA
+               ? launch_seg_cta<OP, LORENZ_RK4_FMA>(C, P, scta, K, Kb, in, out, res, tags, block_ok, st)
                : launch_seg_cta<OP, LORENZ_RK4>(C, P, scta, K, Kb, in, out, res, tags, block_ok, st);
   const int cta = chain_cta(C.lanes, integrator);
   if (integrator == LORENZ_RK4_FMA)

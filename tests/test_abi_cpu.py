@@ -124,7 +124,7 @@ def test_launch_plan_rules(L, monkeypatch):
     assert plan(1024)["kind"] == "wave" and plan(1024)["grid"] * plan(1024)["cta"] >= 1024  # C2
     assert L.lorenz_launch_plan(key, 0, 0, 1)["lanes"] == 1
     fma = L.lorenz_keysetup(b"0123456789abcdef", mode=L.FAST, integrator=L.RK4_FMA)
-    assert L.lorenz_launch_plan(fma, 65536 * 1024, 0, 65536)["kind"] == "wave"
+    assert L.lorenz_launch_plan(fma, 65536 * 1024, 0, 65536)["kind"] == "balanced"
     monkeypatch.setenv("LORENZ_SCHED", "wave")
     assert plan(65536)["kind"] == "wave"
     monkeypatch.setenv("LORENZ_SCHED", "seg")

@@ -56,7 +56,7 @@ CASES = [(160, 0, 3), (160, 0, 4), (161, 300, 3), (200, 1, 5), (257, 1023, 7), (
 
 
 @pytest.mark.parametrize("blocks,tail,slots", CASES)
-@pytest.mark.parametrize("integrator", [L.RK4, L.EULER])
+@pytest.mark.parametrize("integrator", [L.RK4, L.EULER, L.RK4_FMA])
 def test_seg_matches_oracle(sched, blocks, tail, slots, integrator):
     sched(slots=slots)
     n = (blocks - (1 if tail else 0)) * 1024 + tail
