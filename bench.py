@@ -126,6 +126,13 @@ class ClockSampler:
                 stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except OSError:
             self.proc = None
+        # nvidia-smi takes a few hundred ms to start: wait for its first sample so that short timed
+        # regions (C3 at a few steps) are sampled too
+        t0 = time.time()
+        while self.proc and self.proc.poll() is None and time.time() - t0 < 5.0:
+            if os.path.getsize(self.path) > 0:
+                break
+            time.sleep(0.02)
         return self
 
     def __exit__(self, *a):

@@ -252,14 +252,18 @@ cudaError_t launch_seg_cta(const lz::DevConst& C, const lz::SegPlan& P, int cta,
                       : launch_seg<OP, INTEG, 256>(C, P, K, Kb, in, out, res, tags, block_ok, st);
 }
 
+// allow_seg = false: the wave kernel whatever the size — for launches queued back to back on
+// several streams (the host-buffer pipeline), where the next launch's CTAs fill the wave kernel's
+// tail, while the balanced kernel (one CTA per SM, slots assumed to start together) would start
+// its CTAs at staggered times.
 template <int OP>
 cudaError_t launch_chain(const lz::DevConst& C, const lz::DevKey& K, const lz::DevKey* Kb,
                          uint32_t integrator, const uint8_t* in, uint8_t* out, lorenz_result* res,
-                         uint8_t* tags, uint8_t* block_ok, cudaStream_t st) {
+                         uint8_t* tags, uint8_t* block_ok, cudaStream_t st, bool allow_seg = true) {
   if (C.lanes == 0) return cudaSuccess;
   lz::SegPlan P;
   int scta = 0;
-  if (seg_plan(C, integrator, &P, &scta))
+  if (allow_seg && seg_plan(C, integrator, &P, &scta))
     return integrator == LORENZ_EULER
                ? launch_seg_cta<OP, LORENZ_EULER>(C, P, scta, K, Kb, in, out, res, tags, block_ok, st)
            : integrator == LORENZ_RK4_FMA
@@ -480,8 +484,9 @@ lorenz_status lorenz_result_init_async(lorenz_result* res, void* stream) {
   return cuda_ok(cudaGetLastError(), "result_init") ? LORENZ_OK : LORENZ_E_CUDA;
 }
 
-lorenz_status lorenz_encrypt_async(const lorenz_key* k, uint64_t n, uint64_t b0, uint64_t b1,
-                                   const uint8_t* pt, uint8_t* ct, lorenz_result* res, void* stream) {
+static lorenz_status encrypt_async_impl(const lorenz_key* k, uint64_t n, uint64_t b0, uint64_t b1,
+                                        const uint8_t* pt, uint8_t* ct, lorenz_result* res, void* stream,
+                                        bool allow_seg) {
   Trace tr("lorenz_encrypt");
   const KeyImpl* K = impl(k);
   if (!K || !res) return LORENZ_E_ARG;
@@ -492,13 +497,13 @@ lorenz_status lorenz_encrypt_async(const lorenz_key* k, uint64_t n, uint64_t b0,
   const lz::DevConst C = make_const(K, n, b0, b1 - b0);
   const lz::DevKey D = make_devkey(K);
   return cuda_ok(launch_chain<lz::OP_ENC>(C, D, nullptr, K->prm.integrator, pt, ct, res, nullptr, nullptr,
-                                          (cudaStream_t)stream), "encrypt launch")
+                                          (cudaStream_t)stream, allow_seg), "encrypt launch")
              ? LORENZ_OK : LORENZ_E_CUDA;
 }
 
-lorenz_status lorenz_decrypt_async(const lorenz_key* k, uint64_t n, uint64_t b0, uint64_t b1,
-                                   const uint8_t* ct, uint8_t* pt, uint8_t* block_ok, lorenz_result* res,
-                                   void* stream) {
+static lorenz_status decrypt_async_impl(const lorenz_key* k, uint64_t n, uint64_t b0, uint64_t b1,
+                                        const uint8_t* ct, uint8_t* pt, uint8_t* block_ok, lorenz_result* res,
+                                        void* stream, bool allow_seg) {
   Trace tr("lorenz_decrypt");
   const KeyImpl* K = impl(k);
   if (!K || !res) return LORENZ_E_ARG;
@@ -509,7 +514,8 @@ lorenz_status lorenz_decrypt_async(const lorenz_key* k, uint64_t n, uint64_t b0,
   const lz::DevConst C = make_const(K, n, b0, b1 - b0);
   const lz::DevKey D = make_devkey(K);
   cudaStream_t st = (cudaStream_t)stream;
-  if (!cuda_ok(launch_chain<lz::OP_DEC>(C, D, nullptr, K->prm.integrator, ct, pt, res, nullptr, block_ok, st),
+  if (!cuda_ok(launch_chain<lz::OP_DEC>(C, D, nullptr, K->prm.integrator, ct, pt, res, nullptr, block_ok, st,
+                                        allow_seg),
                "decrypt launch"))
     return LORENZ_E_CUDA;
   if (!block_ok && ptb) {
@@ -517,6 +523,17 @@ lorenz_status lorenz_decrypt_async(const lorenz_key* k, uint64_t n, uint64_t b0,
     if (!cuda_ok(cudaGetLastError(), "zero_if_failed")) return LORENZ_E_CUDA;
   }
   return LORENZ_OK;
+}
+
+lorenz_status lorenz_encrypt_async(const lorenz_key* k, uint64_t n, uint64_t b0, uint64_t b1,
+                                   const uint8_t* pt, uint8_t* ct, lorenz_result* res, void* stream) {
+  return encrypt_async_impl(k, n, b0, b1, pt, ct, res, stream, true);
+}
+
+lorenz_status lorenz_decrypt_async(const lorenz_key* k, uint64_t n, uint64_t b0, uint64_t b1,
+                                   const uint8_t* ct, uint8_t* pt, uint8_t* block_ok, lorenz_result* res,
+                                   void* stream) {
+  return decrypt_async_impl(k, n, b0, b1, ct, pt, block_ok, res, stream, true);
 }
 
 lorenz_status lorenz_verify_async(const lorenz_key* k, uint64_t n, uint64_t b0, uint64_t b1, const uint8_t* ct,
@@ -1135,8 +1152,8 @@ static lorenz_status host_range(const lorenz_key* k, uint64_t n, uint64_t B0, ui
         ret = LORENZ_E_CUDA;
         break;
       }
-      ret = decrypt ? lorenz_decrypt_async(k, n, b0, b1, d_in[sl], d_out[sl], d_ok[sl], d_res, st)
-                    : lorenz_encrypt_async(k, n, b0, b1, d_in[sl], d_out[sl], d_res, st);
+      ret = decrypt ? decrypt_async_impl(k, n, b0, b1, d_in[sl], d_out[sl], d_ok[sl], d_res, st, C == 1)
+                    : encrypt_async_impl(k, n, b0, b1, d_in[sl], d_out[sl], d_res, st, C == 1);
       if (ret == LORENZ_OK && ob &&
           !cuda_ok(cudaMemcpyAsync(out_host + ooff, d_out[sl], ob, cudaMemcpyDeviceToHost, st), "D2H"))
         ret = LORENZ_E_CUDA;
