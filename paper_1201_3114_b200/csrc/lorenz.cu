@@ -230,6 +230,10 @@ cudaError_t launch_seg(const lz::DevConst& C, const lz::SegPlan& P, const lz::De
   const size_t bytes = hdr + ((size_t)P.slots + 1) * lz::kSegWords * 32 * 8;
   uint8_t* scr = nullptr;
   cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&scr), bytes, st);
+  if (e == cudaErrorMemoryAllocation) {  // no room for the hand-over scratch: take the wave kernel
+    (void)cudaGetLastError();
+    return cudaErrorNotReady;
+  }
   if (e != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(scr, 0, hdr, st)) == cudaSuccess) {
     uint32_t* ticket = reinterpret_cast<uint32_t*>(scr);
@@ -263,12 +267,15 @@ cudaError_t launch_chain(const lz::DevConst& C, const lz::DevKey& K, const lz::D
   if (C.lanes == 0) return cudaSuccess;
   lz::SegPlan P;
   int scta = 0;
-  if (allow_seg && seg_plan(C, integrator, &P, &scta))
-    return integrator == LORENZ_EULER
-               ? launch_seg_cta<OP, LORENZ_EULER>(C, P, scta, K, Kb, in, out, res, tags, block_ok, st)
-           : integrator == LORENZ_RK4_FMA
-               ? launch_seg_cta<OP, LORENZ_RK4_FMA>(C, P, scta, K, Kb, in, out, res, tags, block_ok, st)
-               : launch_seg_cta<OP, LORENZ_RK4>(C, P, scta, K, Kb, in, out, res, tags, block_ok, st);
+  if (allow_seg && seg_plan(C, integrator, &P, &scta)) {
+    const cudaError_t e =
+        integrator == LORENZ_EULER
+            ? launch_seg_cta<OP, LORENZ_EULER>(C, P, scta, K, Kb, in, out, res, tags, block_ok, st)
+        : integrator == LORENZ_RK4_FMA
+            ? launch_seg_cta<OP, LORENZ_RK4_FMA>(C, P, scta, K, Kb, in, out, res, tags, block_ok, st)
+            : launch_seg_cta<OP, LORENZ_RK4>(C, P, scta, K, Kb, in, out, res, tags, block_ok, st);
+    if (e != cudaErrorNotReady) return e;  // cudaErrorNotReady: scratch allocation failed, fall through
+  }
   const int cta = chain_cta(C.lanes, integrator);
   if (integrator == LORENZ_RK4_FMA)
     return launch_chain_cta<OP, LORENZ_RK4_FMA, 128>(C, K, Kb, in, out, res, tags, block_ok, st);
