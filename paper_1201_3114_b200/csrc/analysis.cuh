@@ -28,12 +28,19 @@ __device__ __forceinline__ void bin_coordinate(uint32_t* h, int c, double v) {
   ip = ip < 0 ? 0 : (ip > 127 ? 127 : ip);
   atomicAdd(&h[(c * 4 + 0) * 128 + (int)ip], 1u);
   const double a = fabs(v);
-  const uint64_t m1 = __double2ull_rz(dmul(a, 100.0));
-  const uint64_t m2 = __double2ull_rz(dmul(a, 10000.0));
-  const uint64_t m3 = __double2ull_rz(dmul(a, 1000000.0));
-  atomicAdd(&h[(c * 4 + 1) * 128 + (int)(m1 % 100)], 1u);
-  atomicAdd(&h[(c * 4 + 2) * 128 + (int)(m2 % 100)], 1u);
-  atomicAdd(&h[(c * 4 + 3) * 128 + (int)(m3 % 100)], 1u);
+  uint32_t d1, d2, d3;
+  if (a < 4000.0) {  // every attractor point (|v| < 64): floor(a 10^6) < 2^32, 32-bit remainders
+    d1 = __double2uint_rz(dmul(a, 100.0)) % 100u;
+    d2 = __double2uint_rz(dmul(a, 10000.0)) % 100u;
+    d3 = __double2uint_rz(dmul(a, 1000000.0)) % 100u;
+  } else {
+    d1 = (uint32_t)(__double2ull_rz(dmul(a, 100.0)) % 100);
+    d2 = (uint32_t)(__double2ull_rz(dmul(a, 10000.0)) % 100);
+    d3 = (uint32_t)(__double2ull_rz(dmul(a, 1000000.0)) % 100);
+  }
+  atomicAdd(&h[(c * 4 + 1) * 128 + (int)d1], 1u);
+  atomicAdd(&h[(c * 4 + 2) * 128 + (int)d2], 1u);
+  atomicAdd(&h[(c * 4 + 3) * 128 + (int)d3], 1u);
 }
 
 template <int INTEG>
