@@ -1121,11 +1121,23 @@ static lorenz_status host_range(const lorenz_key* k, uint64_t n, uint64_t B0, ui
                         : std::max<uint64_t>((inb + kHostChunk - 1) / kHostChunk,
                                              std::min<uint64_t>(8, std::max<uint64_t>(1, units / per)));
   if (C > nbk) C = nbk;
+  // Chunk boundaries. Automatic chunking of 3+ chunks makes the first and the last chunk a quarter
+  // of the others: the first H2D and the last D2H are the only copies nothing overlaps.
+  std::vector<uint64_t> cut(C + 1);
+  {
+    const bool ramp = n_chunks == 0 && C >= 3;
+    const uint64_t units4 = 4 * C - (ramp ? 6 : 0);  // chunk weights in quarters: 1, 4, ..., 4, 1
+    uint64_t acc = 0;
+    for (uint64_t c = 0; c <= C; ++c) {
+      cut[c] = B0 + (uint64_t)((unsigned __int128)nbk * acc / units4);
+      if (c < C) acc += (ramp && (c == 0 || c == C - 1)) ? 1 : 4;
+    }
+  }
   const uint32_t S = (uint32_t)std::min<uint64_t>(C, HostPipe::kStreams);
   const uint64_t Bsz = block_B(K, n);
   uint64_t cap_in = 16, cap_out = 16, cap_blk = 1;  // the largest chunk
   for (uint64_t c = 0; c < C; ++c) {
-    const uint64_t b0 = B0 + nbk * c / C, b1 = B0 + nbk * (c + 1) / C;
+    const uint64_t b0 = cut[c], b1 = cut[c + 1];
     uint64_t cp, cc;
     slice_bytes(K, n, b0, b1, &cp, &cc);
     cap_in = std::max(cap_in, decrypt ? cc : cp);
@@ -1146,7 +1158,7 @@ static lorenz_status host_range(const lorenz_key* k, uint64_t n, uint64_t B0, ui
   if (ret == LORENZ_OK) {
     P.fan_out();
     for (uint64_t c = 0; c < C && ret == LORENZ_OK; ++c) {
-      const uint64_t b0 = B0 + nbk * c / C, b1 = B0 + nbk * (c + 1) / C;
+      const uint64_t b0 = cut[c], b1 = cut[c + 1];
       if (b0 == b1) continue;
       const uint32_t sl = (uint32_t)(c % S);
       cudaStream_t st = P.st[sl];
