@@ -250,7 +250,8 @@ lorenz_status lorenz_power_spectrum(const uint8_t* x, uint32_t H, uint32_t W, do
  * slice starts (same slice convention as the device calls; [0, num_blocks) is the
  * whole message). Host->device copies, kernels and device->host copies are
  * pipelined over `n_chunks` block-aligned chunks (0 -> automatic: at least slice/128 MiB,
- * and up to 8 while each chunk keeps >= 2 warps of 32 blocks per SM sub-partition) on the
+ * and up to 8 while each chunk keeps >= 2 warps of 32 blocks per SM sub-partition, the first
+ * and last of 3+ chunks a quarter of the others; n_chunks > 0: equal chunks) on the
  * current device. Chunk c runs on internal stream c % S, S = min(8, chunks), whose
  * device buffers hold one chunk and are reused in stream order, so device memory is
  * bounded by ~2 x S chunks whatever the slice size (slices larger than HBM work).
