@@ -133,3 +133,31 @@ def test_launch_plan_rules(L, monkeypatch):
     assert p["kind"] == "balanced" and p["slots"] == 3 and p["chunks_per_slot"] == 109
     with pytest.raises(L.LorenzError):
         L.lorenz_launch_plan(key, 1024, 0, 2)
+
+
+def test_launch_plan_mcnaughton_invariants(L, monkeypatch):
+    """For every balanced plan: slots <= units (else a slot would hold less than one unit),
+    chunks_per_slot >= Q = (B+16)/16 (a cut unit's two pieces then never overlap in time),
+    slots * chunks_per_slot covers the U * Q chunk line, and the grid holds every slot."""
+    monkeypatch.delenv("LORENZ_SCHED", raising=False)
+    monkeypatch.delenv("LORENZ_SEG_SLOTS", raising=False)
+    import random
+    rng = random.Random(5)
+    for B in (1024, 2048, 65536):
+        key = L.lorenz_keysetup(b"0123456789abcdef", mode=L.FAST, block_size=B)
+        q = (B + 16 + 15) // 16
+        sizes = [rng.randrange(1, 400_000) for _ in range(200)] + [37888, 37889, 65536, 75776, 113664, 113665]
+        for blocks in sizes:
+            n = blocks * B - rng.randrange(0, B)
+            nb = key.num_blocks(n)
+            b0 = rng.randrange(0, nb) if rng.random() < 0.3 else 0
+            p = L.lorenz_launch_plan(key, n, b0, nb)
+            assert p["lanes"] == nb - b0
+            if p["kind"] == "wave":
+                assert p["grid"] * p["cta"] >= p["lanes"]
+                continue
+            units = -(-p["lanes"] // 32)
+            assert 2 * 592 <= p["slots"] <= units
+            assert p["chunks_per_slot"] >= q
+            assert p["slots"] * p["chunks_per_slot"] >= units * q > p["slots"] * (p["chunks_per_slot"] - 1)
+            assert p["grid"] == 148 and p["cta"] * p["grid"] // 32 >= p["slots"]
