@@ -455,7 +455,8 @@ def main():
         pt_h = torch.from_numpy(msg).pin_memory()
         ct_h = torch.empty(sl.ct_bytes, dtype=torch.uint8).pin_memory()
         t_dev = torch.empty(16, dtype=torch.uint8, device=dev)
-        L.lorenz_encrypt_host(key, n, b0, b1, pt_h, ct_h)  # warm the pool and streams
+        for _ in range(2):  # warm the pool, the streams and the host path
+            L.lorenz_encrypt_host(key, n, b0, b1, pt_h, ct_h)
         times = []
         for _ in range(a.steps):
             barrier()

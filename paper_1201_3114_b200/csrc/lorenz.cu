@@ -1065,11 +1065,13 @@ struct HostPipe {
   static constexpr int kStreams = 8;
   cudaStream_t st[kStreams] = {};
   cudaEvent_t ev[kStreams] = {};
+  cudaEvent_t cp[kStreams] = {};  // "chunk c's H2D done": chains the H2Ds in chunk order
   bool init() {
     keep_pool_cached();  // freed stream-ordered memory stays cached across calls
     for (int i = 0; i < kStreams; ++i) {
       if (!cuda_ok(cudaStreamCreateWithFlags(&st[i], cudaStreamNonBlocking), "stream create")) return false;
       if (!cuda_ok(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming), "event create")) return false;
+      if (!cuda_ok(cudaEventCreateWithFlags(&cp[i], cudaEventDisableTiming), "event create")) return false;
     }
     return true;
   }
@@ -1089,6 +1091,7 @@ struct HostPipe {
     for (int i = 0; i < kStreams; ++i) {
       if (st[i]) cudaStreamDestroy(st[i]);
       if (ev[i]) cudaEventDestroy(ev[i]);
+      if (cp[i]) cudaEventDestroy(cp[i]);
     }
   }
 };
@@ -1167,10 +1170,14 @@ static lorenz_status host_range(const lorenz_key* k, uint64_t n, uint64_t B0, ui
       const uint64_t poff = (b0 - B0) * Bsz, coff = poff + 16 * (b0 - B0);  // offsets inside the slice
       const uint64_t ioff = decrypt ? coff : poff, ooff = decrypt ? poff : coff;
       const uint64_t ib = decrypt ? cc : cp, ob = decrypt ? cp : cc;
+      // H2Ds in chunk order (the copy engines would otherwise share their bandwidth between the
+      // streams' copies and delay the first chunk's kernel)
+      if (c > 0) cudaStreamWaitEvent(st, P.cp[(c - 1) % S], 0);
       if (ib && !cuda_ok(cudaMemcpyAsync(d_in[sl], in_host + ioff, ib, cudaMemcpyHostToDevice, st), "H2D")) {
         ret = LORENZ_E_CUDA;
         break;
       }
+      cudaEventRecord(P.cp[sl], st);
       ret = decrypt ? decrypt_async_impl(k, n, b0, b1, d_in[sl], d_out[sl], d_ok[sl], d_res, st, C == 1)
                     : encrypt_async_impl(k, n, b0, b1, d_in[sl], d_out[sl], d_res, st, C == 1);
       if (ret == LORENZ_OK && ob &&
