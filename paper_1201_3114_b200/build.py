@@ -12,13 +12,16 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(CSRC, "liblorenz.so")
-SOURCES = ["lorenz.cu", "lorenz_io.cu"]
-HEADERS = ["lorenz_device.cuh", "sha256.cuh", "stats.cuh", "analysis.cuh", "spectra.cuh",
+SOURCES = ["lorenz.cu", "lorenz_io.cu", "lorenz_seg.cu"]
+HEADERS = ["lorenz_device.cuh", "sha256.cuh", "stats.cuh", "analysis.cuh", "spectra.cuh", "seg_launch.h",
            os.path.join("..", "..", "include", "lorenz.h")]
+# translation units, compiled in parallel: lorenz_seg.cu once per OP (its kernel instantiations
+# are the bulk of the compile time)
+UNITS = [("lorenz.cu", []), ("lorenz_io.cu", [])] + [("lorenz_seg.cu", [f"-DLZ_SEG_OP={op}"]) for op in range(3)]
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-fmad=false", "-prec-div=true", "-prec-sqrt=true", "-Xptxas", "-v",
-              "-Xcompiler", "-fPIC,-O2,-ffp-contract=off", "-shared"]
+              "-Xcompiler", "-fPIC,-O2,-ffp-contract=off"]
 
 
 def nvcc() -> str:
@@ -35,17 +38,39 @@ def stale() -> bool:
     return any(os.path.getmtime(os.path.join(CSRC, f)) > t for f in SOURCES + HEADERS)
 
 
+def compile_lib(out: str, defines=()) -> str:
+    """nvcc every translation unit to an object (in parallel), then link the shared library.
+    Returns the compilers' stderr (ptxas -v register / spill report)."""
+    import tempfile
+    out = os.path.abspath(out)
+    with tempfile.TemporaryDirectory(prefix="lorenz_build_") as tmp:
+        procs = []
+        for i, (src, extra) in enumerate(UNITS):
+            obj = os.path.join(tmp, f"{i}_{src}.o")
+            cmd = [nvcc()] + NVCC_FLAGS + list(defines) + extra + ["-c", "-o", obj, os.path.join(CSRC, src)]
+            procs.append((obj, cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE,
+                                                     text=True, cwd=CSRC)))
+        log = []
+        for obj, cmd, p in procs:
+            o, e = p.communicate()
+            if p.returncode != 0:
+                raise RuntimeError("nvcc failed: " + " ".join(cmd) + "\n" + o + e)
+            log.append(e)
+        link = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-fPIC", "-o", out]
+        r = subprocess.run(link + [o for o, _, _ in procs], capture_output=True, text=True, cwd=CSRC)
+        if r.returncode != 0:
+            raise RuntimeError("nvcc link failed:\n" + r.stdout + r.stderr)
+    return "".join(log)
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not stale():
         return LIB
-    cmd = [nvcc()] + NVCC_FLAGS + ["-o", LIB] + [os.path.join(CSRC, s) for s in SOURCES]
-    r = subprocess.run(cmd, capture_output=True, text=True, cwd=CSRC)
-    if r.returncode != 0:
-        raise RuntimeError("nvcc failed:\n" + r.stdout + r.stderr)
+    log = compile_lib(LIB)
     if verbose:
-        print(r.stderr)
+        print(log)
     with open(os.path.join(CSRC, "ptxas.log"), "w") as f:
-        f.write(r.stderr)
+        f.write(log)
     build_cli()
     return LIB
 
@@ -65,4 +90,15 @@ def build_cli() -> str:
 
 
 if __name__ == "__main__":
-    print(build(force=True, verbose=True))
+    import argparse
+    ap = argparse.ArgumentParser(description="build liblorenz.so (or a tuning variant of it)")
+    ap.add_argument("-D", dest="defines", action="append", default=[],
+                    help="extra macro for a tuning variant, e.g. -D LZ_SEG_TRACE (needs --out)")
+    ap.add_argument("--out", help="write the variant library here instead of csrc/liblorenz.so")
+    a = ap.parse_args()
+    if a.out:
+        compile_lib(a.out, ["-D" + d for d in a.defines])
+        print(a.out)
+    else:
+        assert not a.defines, "variants (-D) go to --out, never over the product library"
+        print(build(force=True, verbose=True))

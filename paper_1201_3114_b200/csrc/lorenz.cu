@@ -18,6 +18,7 @@
 
 #include "../../include/lorenz.h"
 #include "lorenz_device.cuh"
+#include "seg_launch.h"
 #include "analysis.cuh"
 #include "sha256.cuh"
 #include "spectra.cuh"
@@ -222,40 +223,6 @@ bool seg_plan(const lz::DevConst& C, uint32_t integrator, lz::SegPlan* P, int* c
   return true;
 }
 
-template <int OP, int INTEG, int CTA>
-cudaError_t launch_seg(const lz::DevConst& C, const lz::SegPlan& P, const lz::DevKey& K, const lz::DevKey* Kb,
-                       const uint8_t* in, uint8_t* out, lorenz_result* res, uint8_t* tags, uint8_t* block_ok,
-                       cudaStream_t st) {
-  const size_t hdr = (4 * ((size_t)P.slots + 2) + 15) & ~(size_t)15;  // ticket + S + 1 flags
-  const size_t bytes = hdr + ((size_t)P.slots + 1) * lz::kSegWords * 32 * 8;
-  uint8_t* scr = nullptr;
-  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&scr), bytes, st);
-  if (e == cudaErrorMemoryAllocation) {  // no room for the hand-over scratch: take the wave kernel
-    (void)cudaGetLastError();
-    return cudaErrorNotReady;
-  }
-  if (e != cudaSuccess) return e;
-  if ((e = cudaMemsetAsync(scr, 0, hdr, st)) == cudaSuccess) {
-    uint32_t* ticket = reinterpret_cast<uint32_t*>(scr);
-    const unsigned grid = (unsigned)((P.slots + CTA / 32 - 1) / (CTA / 32));
-    lz::lorenz_chain_seg_kernel<OP, INTEG, CTA><<<grid, CTA, 0, st>>>(
-        C, K, Kb, in, out, res, tags, block_ok, P, ticket, ticket + 1, reinterpret_cast<uint64_t*>(scr + hdr));
-    e = cudaGetLastError();
-  }
-  const cudaError_t f = cudaFreeAsync(scr, st);
-  return e != cudaSuccess ? e : f;
-}
-
-template <int OP, int INTEG>
-cudaError_t launch_seg_cta(const lz::DevConst& C, const lz::SegPlan& P, int cta, const lz::DevKey& K,
-                           const lz::DevKey* Kb, const uint8_t* in, uint8_t* out, lorenz_result* res, uint8_t* tags,
-                           uint8_t* block_ok, cudaStream_t st) {
-  keep_pool_cached();
-  return cta == 512   ? launch_seg<OP, INTEG, 512>(C, P, K, Kb, in, out, res, tags, block_ok, st)
-         : cta == 384 ? launch_seg<OP, INTEG, 384>(C, P, K, Kb, in, out, res, tags, block_ok, st)
-                      : launch_seg<OP, INTEG, 256>(C, P, K, Kb, in, out, res, tags, block_ok, st);
-}
-
 // allow_seg = false: the wave kernel whatever the size — for launches queued back to back on
 // several streams (the host-buffer pipeline), where the next launch's CTAs fill the wave kernel's
 // tail, while the balanced kernel (one CTA per SM, slots assumed to start together) would start
@@ -268,12 +235,8 @@ cudaError_t launch_chain(const lz::DevConst& C, const lz::DevKey& K, const lz::D
   lz::SegPlan P;
   int scta = 0;
   if (allow_seg && seg_plan(C, integrator, &P, &scta)) {
-    const cudaError_t e =
-        integrator == LORENZ_EULER
-            ? launch_seg_cta<OP, LORENZ_EULER>(C, P, scta, K, Kb, in, out, res, tags, block_ok, st)
-        : integrator == LORENZ_RK4_FMA
-            ? launch_seg_cta<OP, LORENZ_RK4_FMA>(C, P, scta, K, Kb, in, out, res, tags, block_ok, st)
-            : launch_seg_cta<OP, LORENZ_RK4>(C, P, scta, K, Kb, in, out, res, tags, block_ok, st);
+    keep_pool_cached();
+    const cudaError_t e = lz::launch_seg_op<OP>(C, P, scta, integrator, K, Kb, in, out, res, tags, block_ok, st);
     if (e != cudaErrorNotReady) return e;  // cudaErrorNotReady: scratch allocation failed, fall through
   }
   const int cta = chain_cta(C.lanes, integrator);
@@ -351,15 +314,6 @@ void set_last_error(const std::string& s) { g_err = s; }  // shared with lorenz_
 // ======================================================================== C ABI
 extern "C" {
 
-#ifdef LZ_SEG_TRACE
-// Tuning builds only: copy the per-slot timeline (4096 x 8 u64) out, then zero it (slots with no
-// work record nothing, so rows of an earlier launch would otherwise survive).
-int lorenz_debug_seg_trace(unsigned long long* host) {
-  if (cudaMemcpyFromSymbol(host, lz::g_seg_trace, sizeof lz::g_seg_trace) != cudaSuccess) return 1;
-  static unsigned long long zeros[4096 * 8];
-  return cudaMemcpyToSymbol(lz::g_seg_trace, zeros, sizeof zeros) == cudaSuccess ? 0 : 1;
-}
-#endif
 
 int lorenz_abi_version(void) { return LORENZ_ABI_VERSION; }
 

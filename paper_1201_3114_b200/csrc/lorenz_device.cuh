@@ -772,7 +772,7 @@ __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
 }
 
 #ifdef LZ_SEG_TRACE  // tuning builds only (tools/seg_trace.py): per-slot timeline
-__device__ unsigned long long g_seg_trace[4096 * 8];
+static __device__ unsigned long long g_seg_trace[4096 * 8];  // per translation unit
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -864,7 +864,7 @@ __global__ void __launch_bounds__(CTA, 1)
 
 // Zero the plaintext slice if the launch found an integrity failure (async decrypt
 // without per-block verdicts: unauthenticated plaintext is never released).
-__global__ void zero_if_failed_kernel(const lorenz_result* __restrict__ res, uint8_t* __restrict__ pt,
+static __global__ void zero_if_failed_kernel(const lorenz_result* __restrict__ res, uint8_t* __restrict__ pt,
                                       uint64_t nbytes) {
   if (!(res->status & ST_INTEGRITY)) return;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nbytes;
@@ -872,7 +872,7 @@ __global__ void zero_if_failed_kernel(const lorenz_result* __restrict__ res, uin
     pt[i] = 0;
 }
 
-__global__ void result_init_kernel(lorenz_result* res) {
+static __global__ void result_init_kernel(lorenz_result* res) {
   if (threadIdx.x == 0) {
     *reinterpret_cast<unsigned long long*>(res->tag_xor) = 0;
     *reinterpret_cast<unsigned long long*>(res->tag_xor + 8) = 0;

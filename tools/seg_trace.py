@@ -1,9 +1,10 @@
 """Timeline of the balanced (McNaughton) chain kernel, one row per warp slot (1 GPU).
 
-Builds nothing itself: run with LORENZ_LIB pointing at a liblorenz.so compiled with
--DLZ_SEG_TRACE (tools/seg_trace.sh does both). For one encrypt launch of each size it
-prints the slot count, the kernel time, how long slots waited for their cut unit's first
-piece, and when slots finished relative to the kernel's end (the tail), per SM sub-partition.
+Builds nothing itself: run it with LORENZ_LIB pointing at a tuning build of the library,
+`python paper_1201_3114_b200/build.py -D LZ_SEG_TRACE --out tools/variants/liblorenz_trace.so`.
+For one encrypt launch of each size it prints the slot count, the kernel time, how long slots
+waited for their cut unit's first piece, and when slots finished relative to the kernel's end
+(the tail), per SM sub-partition.
 
 Usage: LORENZ_LIB=tools/variants/liblorenz_trace.so python tools/seg_trace.py --kib 65536 100000
 """
