@@ -57,3 +57,45 @@ def test_random_configurations(seed):
         assert st == L.OK and fb == -1
         if hi > lo:
             assert np.array_equal(back[:hi - lo].cpu().numpy(), msg[lo:hi])
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_random_configurations_balanced_kernel(seed, monkeypatch):
+    """The same parity through the balanced kernel, forced onto a random number of warp slots
+    (so units are cut at random chunk positions): FAST messages of 33-420 blocks, random block
+    sizes, block ranges, integrators, step sizes and Step-3 variants."""
+    monkeypatch.setenv("LORENZ_SCHED", "seg")
+    rng = random.Random(7000 + seed)
+    for _ in range(25):
+        B = rng.choice([1024, 1040, 1024 + 16 * rng.randrange(1, 64)])
+        blocks = rng.randrange(33, 420)
+        n = blocks * B - rng.choice([0, 0, rng.randrange(1, B)])
+        integ = rng.choice([L.RK4, L.RK4, L.EULER, L.RK4_FMA])
+        kw = dict(mode=L.FAST, n_it=rng.randrange(1, 9), dt_code=rng.randrange(3) if integ == L.EULER
+                  else rng.randrange(4), block_size=B, integrator=integ, variant=rng.choice([0, 0, 1, 2, 4, 5]))
+        pw = rng.randbytes(rng.randrange(3, 40))
+        msg = np.frombuffer(rng.randbytes(n), np.uint8)
+        key = L.lorenz_keysetup(pw, **kw)
+        nb = key.num_blocks(n)
+        b0 = rng.choice([0, rng.randrange(nb // 2)])
+        b1 = nb if rng.random() < 0.5 else rng.randrange(b0 + 1, nb + 1)
+        units = -(-(b1 - b0) // 32)
+        monkeypatch.setenv("LORENZ_SEG_SLOTS", str(rng.randrange(1, units + 1)))
+        p = key.params
+        prm = oracle.params(mode=p.mode, n_it=p.n_it, dt_code=p.dt_code, block_size=p.block_size,
+                            integrator=p.integrator, variant=p.variant)
+        want, _ = oracle.encrypt(pw, msg, prm, b0=b0, b1=b1)
+        lo, hi = b0 * B, min(n, b1 * B)
+        pt = torch.from_numpy(msg[lo:hi].copy()).to(DEV)
+        ct = torch.empty(hi - lo + 16 * (b1 - b0), dtype=torch.uint8, device=DEV)
+        assert L.lorenz_launch_plan(key, n, b0, b1)["kind"] == "balanced"
+        tag = L.lorenz_encrypt(key, n, b0, b1, pt, ct)
+        clo = lo + 16 * b0
+        got = ct.cpu().numpy()
+        assert np.array_equal(got, want[clo:clo + got.size]), (kw, n, b0, b1)
+        tags = [want[min(n, (b + 1) * B) + 16 * b: min(n, (b + 1) * B) + 16 * b + 16] for b in range(b0, b1)]
+        assert np.bitwise_xor.reduce(np.stack(tags), axis=0).tobytes() == tag
+        back = torch.empty(hi - lo, dtype=torch.uint8, device=DEV)
+        st, fb = L.lorenz_decrypt(key, n, b0, b1, ct, back)
+        assert st == L.OK and fb == -1
+        assert np.array_equal(back.cpu().numpy(), msg[lo:hi])
