@@ -249,10 +249,10 @@ lorenz_status lorenz_power_spectrum(const uint8_t* x, uint32_t H, uint32_t W, do
  * blocks [b0,b1) of an n-byte message; pt_host / ct_host are HOST pointers to the
  * slice starts (same slice convention as the device calls; [0, num_blocks) is the
  * whole message). Host->device copies, kernels and device->host copies are
- * pipelined over `n_chunks` block-aligned chunks (0 -> automatic: at least slice/128 MiB,
- * and up to 8 while each chunk keeps >= 2 warps of 32 blocks per SM sub-partition, the first
- * and last of 3+ chunks a quarter of the others; n_chunks > 0: equal chunks) on the
- * current device. Chunk c runs on internal stream c % S, S = min(8, chunks), whose
+ * pipelined over `n_chunks` block-aligned chunks (0 -> automatic: first and last chunk the
+ * smallest that keep 2 warps of 32 blocks per SM sub-partition, middle chunks <= 128 MiB, one
+ * chunk below twice that minimum; n_chunks > 0: equal chunks) on the current device. Chunk
+ * kernels run one at a time, each overlapped with the neighbouring chunks' copies. Chunk c runs on internal stream c % S, S = min(8, chunks), whose
  * device buffers hold one chunk and are reused in stream order, so device memory is
  * bounded by ~2 x S chunks whatever the slice size (slices larger than HBM work).
  * Pinned host memory gives overlapped copies; pageable memory works but copies

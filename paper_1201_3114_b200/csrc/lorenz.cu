@@ -223,18 +223,14 @@ bool seg_plan(const lz::DevConst& C, uint32_t integrator, lz::SegPlan* P, int* c
   return true;
 }
 
-// allow_seg = false: the wave kernel whatever the size — for launches queued back to back on
-// several streams (the host-buffer pipeline), where the next launch's CTAs fill the wave kernel's
-// tail, while the balanced kernel (one CTA per SM, slots assumed to start together) would start
-// its CTAs at staggered times.
 template <int OP>
 cudaError_t launch_chain(const lz::DevConst& C, const lz::DevKey& K, const lz::DevKey* Kb,
                          uint32_t integrator, const uint8_t* in, uint8_t* out, lorenz_result* res,
-                         uint8_t* tags, uint8_t* block_ok, cudaStream_t st, bool allow_seg = true) {
+                         uint8_t* tags, uint8_t* block_ok, cudaStream_t st) {
   if (C.lanes == 0) return cudaSuccess;
   lz::SegPlan P;
   int scta = 0;
-  if (allow_seg && seg_plan(C, integrator, &P, &scta)) {
+  if (seg_plan(C, integrator, &P, &scta)) {
     keep_pool_cached();
     const cudaError_t e = lz::launch_seg_op<OP>(C, P, scta, integrator, K, Kb, in, out, res, tags, block_ok, st);
     if (e != cudaErrorNotReady) return e;  // cudaErrorNotReady: scratch allocation failed, fall through
@@ -445,9 +441,8 @@ lorenz_status lorenz_result_init_async(lorenz_result* res, void* stream) {
   return cuda_ok(cudaGetLastError(), "result_init") ? LORENZ_OK : LORENZ_E_CUDA;
 }
 
-static lorenz_status encrypt_async_impl(const lorenz_key* k, uint64_t n, uint64_t b0, uint64_t b1,
-                                        const uint8_t* pt, uint8_t* ct, lorenz_result* res, void* stream,
-                                        bool allow_seg) {
+lorenz_status lorenz_encrypt_async(const lorenz_key* k, uint64_t n, uint64_t b0, uint64_t b1,
+                                   const uint8_t* pt, uint8_t* ct, lorenz_result* res, void* stream) {
   Trace tr("lorenz_encrypt");
   const KeyImpl* K = impl(k);
   if (!K || !res) return LORENZ_E_ARG;
@@ -458,13 +453,13 @@ static lorenz_status encrypt_async_impl(const lorenz_key* k, uint64_t n, uint64_
   const lz::DevConst C = make_const(K, n, b0, b1 - b0);
   const lz::DevKey D = make_devkey(K);
   return cuda_ok(launch_chain<lz::OP_ENC>(C, D, nullptr, K->prm.integrator, pt, ct, res, nullptr, nullptr,
-                                          (cudaStream_t)stream, allow_seg), "encrypt launch")
+                                          (cudaStream_t)stream), "encrypt launch")
              ? LORENZ_OK : LORENZ_E_CUDA;
 }
 
-static lorenz_status decrypt_async_impl(const lorenz_key* k, uint64_t n, uint64_t b0, uint64_t b1,
-                                        const uint8_t* ct, uint8_t* pt, uint8_t* block_ok, lorenz_result* res,
-                                        void* stream, bool allow_seg) {
+lorenz_status lorenz_decrypt_async(const lorenz_key* k, uint64_t n, uint64_t b0, uint64_t b1,
+                                   const uint8_t* ct, uint8_t* pt, uint8_t* block_ok, lorenz_result* res,
+                                   void* stream) {
   Trace tr("lorenz_decrypt");
   const KeyImpl* K = impl(k);
   if (!K || !res) return LORENZ_E_ARG;
@@ -475,8 +470,7 @@ static lorenz_status decrypt_async_impl(const lorenz_key* k, uint64_t n, uint64_
   const lz::DevConst C = make_const(K, n, b0, b1 - b0);
   const lz::DevKey D = make_devkey(K);
   cudaStream_t st = (cudaStream_t)stream;
-  if (!cuda_ok(launch_chain<lz::OP_DEC>(C, D, nullptr, K->prm.integrator, ct, pt, res, nullptr, block_ok, st,
-                                        allow_seg),
+  if (!cuda_ok(launch_chain<lz::OP_DEC>(C, D, nullptr, K->prm.integrator, ct, pt, res, nullptr, block_ok, st),
                "decrypt launch"))
     return LORENZ_E_CUDA;
   if (!block_ok && ptb) {
@@ -484,17 +478,6 @@ static lorenz_status decrypt_async_impl(const lorenz_key* k, uint64_t n, uint64_
     if (!cuda_ok(cudaGetLastError(), "zero_if_failed")) return LORENZ_E_CUDA;
   }
   return LORENZ_OK;
-}
-
-lorenz_status lorenz_encrypt_async(const lorenz_key* k, uint64_t n, uint64_t b0, uint64_t b1,
-                                   const uint8_t* pt, uint8_t* ct, lorenz_result* res, void* stream) {
-  return encrypt_async_impl(k, n, b0, b1, pt, ct, res, stream, true);
-}
-
-lorenz_status lorenz_decrypt_async(const lorenz_key* k, uint64_t n, uint64_t b0, uint64_t b1,
-                                   const uint8_t* ct, uint8_t* pt, uint8_t* block_ok, lorenz_result* res,
-                                   void* stream) {
-  return decrypt_async_impl(k, n, b0, b1, ct, pt, block_ok, res, stream, true);
 }
 
 lorenz_status lorenz_verify_async(const lorenz_key* k, uint64_t n, uint64_t b0, uint64_t b1, const uint8_t* ct,
@@ -1014,18 +997,20 @@ lorenz_status lorenz_histograms(const uint8_t* a, const lorenz_span* spans, uint
 // ---------------------------------------------------------------- host-buffer end to end
 namespace {
 struct HostPipe {
-  // one stream per chunk (up to 8): a chunk's kernel starts when its own H2D lands and
-  // the chunks' grids run concurrently, so small chunks never serialise behind each other
+  // one stream per chunk (up to 8): chunk c's H2D, kernel and D2H are stream-ordered; events
+  // chain the H2Ds and the kernels across streams in chunk order, so copies overlap kernels
   static constexpr int kStreams = 8;
   cudaStream_t st[kStreams] = {};
   cudaEvent_t ev[kStreams] = {};
   cudaEvent_t cp[kStreams] = {};  // "chunk c's H2D done": chains the H2Ds in chunk order
+  cudaEvent_t kd[kStreams] = {};  // "chunk c's kernel done": chains the kernels in chunk order
   bool init() {
     keep_pool_cached();  // freed stream-ordered memory stays cached across calls
     for (int i = 0; i < kStreams; ++i) {
       if (!cuda_ok(cudaStreamCreateWithFlags(&st[i], cudaStreamNonBlocking), "stream create")) return false;
       if (!cuda_ok(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming), "event create")) return false;
       if (!cuda_ok(cudaEventCreateWithFlags(&cp[i], cudaEventDisableTiming), "event create")) return false;
+      if (!cuda_ok(cudaEventCreateWithFlags(&kd[i], cudaEventDisableTiming), "event create")) return false;
     }
     return true;
   }
@@ -1046,6 +1031,7 @@ struct HostPipe {
       if (st[i]) cudaStreamDestroy(st[i]);
       if (ev[i]) cudaEventDestroy(ev[i]);
       if (cp[i]) cudaEventDestroy(cp[i]);
+      if (kd[i]) cudaEventDestroy(kd[i]);
     }
   }
 };
@@ -1054,9 +1040,8 @@ constexpr uint64_t kHostChunk = 128ull << 20;  // upper bound of an automatic ho
 }  // namespace
 
 // Blocks [B0,B1) from host slices: chunked H2D -> kernel -> D2H over HostPipe's streams.
-// The slice is cut into block-aligned chunks (default: at most ~128 MiB each, and up to 8
-// while each chunk still fills the SMs); chunk c runs on slot c % S (S = min(8, chunks)), each slot owning a
-// stream and device buffers sized for one chunk. Chunk c + S reuses the slot's buffers only
+// The slice is cut into block-aligned chunks (plan below); chunk c runs on slot c % S
+// (S = min(8, chunks)), each slot owning a stream and device buffers sized for one chunk. Chunk c + S reuses the slot's buffers only
 // after chunk c's D2H (same stream), so the host never waits and device memory stays bounded
 // (≈ 8 x 2 x 128 MiB) whatever the message size: messages larger than HBM work.
 static lorenz_status host_range(const lorenz_key* k, uint64_t n, uint64_t B0, uint64_t B1, const uint8_t* in_host,
@@ -1070,28 +1055,36 @@ static lorenz_status host_range(const lorenz_key* k, uint64_t n, uint64_t B0, ui
   lorenz_status ret = check_range(K, n, B0, B1, in_host, inb, out_host, outb);
   if (ret != LORENZ_OK || B0 == B1) return ret;
   const uint64_t nbk = B1 - B0;
-  // automatic: chunks of at most kHostChunk, and up to 8 (for copy/compute overlap) as long as
-  // each keeps >= 2 warps of chains per SM sub-partition, the least a launch needs to keep the
-  // FP64 pipe busy (C3, 64 MiB: one chunk; 8 chunks of 8 MiB ran at 82 % of the device rate)
-  const uint64_t units = (nbk + 31) / 32, per = 8 * (uint64_t)sm_count();
-  uint64_t C = n_chunks ? n_chunks
-                        : std::max<uint64_t>((inb + kHostChunk - 1) / kHostChunk,
-                                             std::min<uint64_t>(8, std::max<uint64_t>(1, units / per)));
-  if (C > nbk) C = nbk;
-  // Chunk boundaries. Automatic chunking of 3+ chunks makes the first and the last chunk a quarter
-  // of the others: the first H2D and the last D2H are the only copies nothing overlaps.
-  std::vector<uint64_t> cut(C + 1);
-  {
-    const bool ramp = n_chunks == 0 && C >= 3;
-    const uint64_t units4 = 4 * C - (ramp ? 6 : 0);  // chunk weights in quarters: 1, 4, ..., 4, 1
-    uint64_t acc = 0;
-    for (uint64_t c = 0; c <= C; ++c) {
-      cut[c] = B0 + (uint64_t)((unsigned __int128)nbk * acc / units4);
-      if (c < C) acc += (ramp && (c == 0 || c == C - 1)) ? 1 : 4;
-    }
-  }
-  const uint32_t S = (uint32_t)std::min<uint64_t>(C, HostPipe::kStreams);
   const uint64_t Bsz = block_B(K, n);
+  // Chunk plan: block boundaries cut[0..C]. The chunk kernels run one after another (each is a
+  // launch of its own, so the library's schedule choice applies to it), overlapped with the next
+  // chunk's H2D and the previous chunk's D2H. n_chunks > 0: C equal chunks. Automatic: the first
+  // and the last chunk — whose copies nothing overlaps — are the smallest that still give 2 warps
+  // per SM sub-partition (8 x SMs units of 32 blocks); the middle is cut into chunks of at most
+  // kHostChunk bytes (and at least that minimum). Slices under two minimal chunks: one chunk.
+  std::vector<uint64_t> cut;
+  if (n_chunks) {
+    const uint64_t C = std::min<uint64_t>(n_chunks, nbk);
+    for (uint64_t c = 0; c <= C; ++c) cut.push_back(B0 + (uint64_t)((unsigned __int128)nbk * c / C));
+  } else {
+    const uint64_t edge = 32 * 8 * (uint64_t)sm_count();
+    cut.push_back(B0);
+    if (nbk >= 2 * edge) {
+      const uint64_t mid = nbk - 2 * edge;
+      if (mid < edge) {
+        cut.push_back(B0 + nbk / 2);
+      } else {
+        const uint64_t maxb = std::max<uint64_t>(edge, kHostChunk / std::max<uint64_t>(Bsz, 1));
+        const uint64_t M = (mid + maxb - 1) / maxb;
+        cut.push_back(B0 + edge);
+        for (uint64_t i = 1; i < M; ++i) cut.push_back(B0 + edge + (uint64_t)((unsigned __int128)mid * i / M));
+        cut.push_back(B1 - edge);
+      }
+    }
+    cut.push_back(B1);
+  }
+  const uint64_t C = cut.size() - 1;
+  const uint32_t S = (uint32_t)std::min<uint64_t>(C, HostPipe::kStreams);
   uint64_t cap_in = 16, cap_out = 16, cap_blk = 1;  // the largest chunk
   for (uint64_t c = 0; c < C; ++c) {
     const uint64_t b0 = cut[c], b1 = cut[c + 1];
@@ -1132,8 +1125,10 @@ static lorenz_status host_range(const lorenz_key* k, uint64_t n, uint64_t B0, ui
         break;
       }
       cudaEventRecord(P.cp[sl], st);
-      ret = decrypt ? decrypt_async_impl(k, n, b0, b1, d_in[sl], d_out[sl], d_ok[sl], d_res, st, C == 1)
-                    : encrypt_async_impl(k, n, b0, b1, d_in[sl], d_out[sl], d_res, st, C == 1);
+      if (c > 0) cudaStreamWaitEvent(st, P.kd[(c - 1) % S], 0);  // kernels in chunk order, one at a time
+      ret = decrypt ? lorenz_decrypt_async(k, n, b0, b1, d_in[sl], d_out[sl], d_ok[sl], d_res, st)
+                    : lorenz_encrypt_async(k, n, b0, b1, d_in[sl], d_out[sl], d_res, st);
+      cudaEventRecord(P.kd[sl], st);
       if (ret == LORENZ_OK && ob &&
           !cuda_ok(cudaMemcpyAsync(out_host + ooff, d_out[sl], ob, cudaMemcpyDeviceToHost, st), "D2H"))
         ret = LORENZ_E_CUDA;
