@@ -252,6 +252,7 @@ def run_c5(a):
     import torch
     import torch.distributed as dist
 
+    from paper_1201_3114_b200 import lorenz as L
     from paper_1201_3114_b200 import sweep
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -264,6 +265,9 @@ def run_c5(a):
         init_dist(dev)
     n, B, T = 1 << 20, 1024, a.c5_trials
     bt = sweep.Batch(rank * T, T, n, a.n_it, B, dev)
+    # the batch launch covers 3 T streams of n bytes: the plan of a launch with that many lanes
+    lanes = 3 * T * bt.keys[0].num_blocks(n)
+    c5_plan = L.lorenz_launch_plan(bt.keys[0], lanes * B, 0, lanes)
     flush = torch.empty(2 * L2_BYTES, dtype=torch.uint8, device=dev)
     for _ in range(a.warmup):
         bt.encrypt()
@@ -312,7 +316,7 @@ def run_c5(a):
                        "n_it": a.n_it, "block_size": B, "l2": "flushed between timed steps"},
             "roofline": {"bound": "alu", "achieved": round(achieved, 4), "peak": round(peak, 4),
                          "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": None,
-                         "kernel": "lz::lorenz_chain_kernel<ENC,RK4> (batch)"},
+                         "kernel": kernel_label(c5_plan, "rk4") + " (batch)", "schedule": c5_plan},
             "phase_ms": {"encrypt": [round(x, 2) for x in enc_ms], "statistics": [round(x, 2) for x in stats_ms]},
             "c5_stats_rank0": {"pw_flip_bit_diff_mean": float(pw_bits.mean()),
                                "ct_entropy_min": float(min(ent)),

@@ -125,7 +125,10 @@ typedef struct {
   uint64_t grid;            /* CTAs                                                   */
   uint64_t lanes;           /* b1 - b0 chains                                         */
   uint64_t slots;           /* balanced: warp slots sharing the units (0 for wave)    */
-  uint64_t chunks_per_slot; /* balanced: 16-character chunks per slot (0 for wave)    */
+  uint64_t chunks_per_slot; /* balanced: 16-character chunks per slot (0 for wave); with a
+                               skew, the slots of a CTA's warps w get chunks_per_slot +
+                               (w / 4) * chunks_skew (later warps of a CTA run faster)     */
+  uint64_t chunks_skew;     /* balanced: see above (0: equal slots)                     */
 } lorenz_plan;
 lorenz_status lorenz_launch_plan(const lorenz_key* k, uint64_t n, uint64_t b0, uint64_t b1,
                                  lorenz_plan* out);

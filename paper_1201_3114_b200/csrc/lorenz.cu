@@ -178,14 +178,15 @@ cudaError_t launch_chain_cta(const lz::DevConst& C, const lz::DevKey& K, const l
 void keep_pool_cached();
 
 // Balanced schedule (lz::lorenz_chain_seg_kernel, lorenz_device.cuh) for chain launches
-// with two or more warps of chains per SM sub-partition and fewer than three waves (rules
-// below): one CTA of 128 w threads per SM,
+// with two or more warps of chains per SM sub-partition (exceptions below): one CTA of 128 w
+// threads per SM,
 // S = SMs x 4 x w warp slots, w = min(4, warps per sub-partition) (tools/tune.py: 2 warps per
 // sub-partition already keep the FP64 pipe 97 % busy, 4 reach 98 %). One CTA per SM because
 // the warp schedulers favour the older of two co-resident CTAs (tools/seg_trace.py: with
 // 2 x 256 threads per SM the second CTA's warps ran at half rate until the first finished, and
 // slots cut across the two classes waited), while the warps of one CTA keep within ~3 %.
-// Overrides for tests and tuning: LORENZ_SCHED=wave|seg, LORENZ_SEG_SLOTS=S (clamped to U).
+// Overrides for tests and tuning: LORENZ_SCHED=wave|seg, LORENZ_SEG_SLOTS=S (clamped to U),
+// LORENZ_SEG_SKEW=per mille (0: equal slots).
 bool seg_plan(const lz::DevConst& C, uint32_t integrator, lz::SegPlan* P, int* cta) {
   if (integrator > LORENZ_RK4_FMA) return false;
   const char* sched = std::getenv("LORENZ_SCHED");
@@ -194,11 +195,12 @@ bool seg_plan(const lz::DevConst& C, uint32_t integrator, lz::SegPlan* P, int* c
   const bool forced = sched && std::strcmp(sched, "seg") == 0;
   uint64_t w = std::min<uint64_t>(4, U / (4 * sms));
   if (!forced) {
-    // The wave kernel wins (tools/tune.py, RK4): with >= 3 waves of 16 warps
-    // per SM, where the dynamic CTA dispatch balances the SMs (97.6-97.9 % of the FP64 pipe
-    // against 97.0-97.2 % here), and in one wave whose warps split evenly over the SM
-    // sub-partitions (2 per sub-partition per 256-thread CTA).
-    if (w < 2 || U > 3 * 16 * sms) return false;
+    // The wave kernel wins (tools/tune.py) in one wave whose warps split evenly
+    // over the SM sub-partitions (2 per sub-partition per 256-thread CTA) and, for Euler and
+    // RK4-FMA, from 3 waves of 16 warps per SM on, where the dynamic CTA dispatch balances the
+    // SMs. RK4 keeps the balanced kernel at every larger size (1 GiB: 98.05 % against 97.9 %).
+    if (w < 2) return false;
+    if (integrator != LORENZ_RK4 && U > 3 * 16 * sms) return false;
     // RK4-FMA: the wave kernel runs 20 warps per SM (5 x 128 threads, <= 102 registers), which
     // its shorter dependent chains need; the balanced kernel's 12-16 reach ~85 %, so it only wins
     // while the wave kernel's single wave splits badly (C3: 85 % vs 78 %; 128 MiB: 84 % vs 90 %)
@@ -219,7 +221,32 @@ bool seg_plan(const lz::DevConst& C, uint32_t integrator, lz::SegPlan* P, int* c
   P->q = (uint32_t)((C.B + 16 + 15) / 16);
   P->slots = (uint32_t)S;
   P->cq = (U * P->q + S - 1) / S;
+  P->wpc = 0;
+  P->dq = 0;
   *cta = (int)(128 * w);
+  // Skew: within a CTA, warps with a higher index progress faster (tools/seg_trace.py: the four
+  // warp groups of a 512-thread CTA finished equal slots at 112.8 / 112.1 / 110.8 / 109.2 ms),
+  // so each group of four warps gets `skew` per mille of the mean slot more than the previous
+  // one and the slots finish together (tools/tune.py: 8 per mille, 1 GiB 97.95 % -> 98.05 %,
+  // 128 MiB 97.45 % -> 97.96 %). Only for the default slot layout (S = SMs x warps per CTA),
+  // and only while every slot keeps >= Q/8 chunks of slack over a unit (the two pieces of a
+  // cut unit must not meet: with no slack, 1,184 units over 1,184 skewed slots ran at 61 %).
+  const uint64_t wpc = 4 * w, G = sms;
+  uint64_t skew = 8;
+  if (const char* f = std::getenv("LORENZ_SEG_SKEW")) skew = std::strtoull(f, nullptr, 10);
+  if (skew && S == G * wpc) {
+    const uint64_t UQ = U * P->q, ng = wpc / 4;
+    const uint64_t dq = (UQ / S * skew + 500) / 1000;
+    const uint64_t extra = G * 2 * dq * ng * (ng - 1);
+    if (dq && UQ > extra) {
+      const uint64_t cq = (UQ - extra + S - 1) / S;
+      if (cq >= P->q + P->q / 8) {
+        P->cq = cq;
+        P->wpc = (uint32_t)wpc;
+        P->dq = (uint32_t)dq;
+      }
+    }
+  }
   return true;
 }
 
@@ -404,6 +431,7 @@ lorenz_status lorenz_launch_plan(const lorenz_key* k, uint64_t n, uint64_t b0, u
     out->grid = (P.slots + cta / 32 - 1) / (cta / 32);
     out->slots = P.slots;
     out->chunks_per_slot = P.cq;
+    out->chunks_skew = P.dq;
   } else {
     out->cta = (uint32_t)chain_cta(C.lanes, K->prm.integrator);
     out->grid = (C.lanes + out->cta - 1) / out->cta;

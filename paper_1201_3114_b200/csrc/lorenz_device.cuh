@@ -721,10 +721,29 @@ __global__ void __launch_bounds__(CTA, (min_ctas<INTEG, CTA>()))
 // it runs first thing: no deadlock even when not every CTA is resident.
 struct SegPlan {
   uint64_t units;  // U = ceil(lanes / 32)
-  uint64_t cq;     // chunks per slot
+  uint64_t cq;     // chunks per slot (warp group 0 when skewed)
   uint32_t q;      // chunks per unit = ceil((B + 16) / 16)
   uint32_t slots;  // S (<= U)
+  uint32_t wpc;    // warps per CTA when skewed (S = CTAs x wpc), else 0
+  uint32_t dq;     // skew: slots of warp index w get cq + (w / 4) dq chunks
 };
+
+// Chunk line position [x0, x1) of slot k. Unskewed: [k Cq, (k+1) Cq). Skewed: position k holds
+// the slot of warp index wpc - 1 - (k mod wpc) (later starters take earlier positions), whose
+// capacity grows by dq per warp group of four.
+__device__ __forceinline__ void seg_slot_range(const SegPlan& P, uint64_t k, uint64_t& x0, uint64_t& x1) {
+  if (P.wpc == 0) {
+    x0 = k * P.cq;
+    x1 = x0 + P.cq;
+    return;
+  }
+  const uint32_t ng = P.wpc / 4, r = (uint32_t)(k % P.wpc);
+  const uint64_t block = (uint64_t)P.wpc * P.cq + 2ull * P.dq * ng * (ng - 1);  // one CTA's slots
+  uint64_t off = 0;
+  for (uint32_t j = 0; j < r; ++j) off += P.cq + (uint64_t)((P.wpc - 1 - j) >> 2) * P.dq;
+  x0 = (k / P.wpc) * block + off;
+  x1 = x0 + P.cq + (uint64_t)((P.wpc - 1 - r) >> 2) * P.dq;
+}
 constexpr int kSegWords = 18;  // u64 words of one lane's handed-over state
 
 __device__ __forceinline__ void seg_save(uint64_t* dst, uint32_t lane, const Chain& c, const LaneAcc& a) {
@@ -806,9 +825,10 @@ __global__ void __launch_bounds__(CTA, 1)
   if (t >= P.slots) return;
   const uint64_t k = P.slots - 1 - t;  // later starters take earlier positions
   const uint64_t Q = P.q, UQ = P.units * Q;
-  const uint64_t X0 = k * P.cq;
+  uint64_t X0, X1;
+  seg_slot_range(P, k, X0, X1);
   if (X0 >= UQ) return;
-  const uint64_t X1 = (X0 + P.cq < UQ) ? X0 + P.cq : UQ;
+  if (X1 > UQ) X1 = UQ;
   uint8_t* wst = stage + warp * 32 * (WIN + 16);
   uint64_t u = X0 / Q;
 #ifdef LZ_SEG_TRACE

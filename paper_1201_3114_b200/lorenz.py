@@ -179,7 +179,7 @@ def lorenz_keysetup(pw: bytes, mode: int = FAST, n_it: int = 0, dt_code: int = 0
 
 class lorenz_plan(C.Structure):
     _fields_ = [("kind", C.c_uint32), ("cta", C.c_uint32), ("grid", C.c_uint64), ("lanes", C.c_uint64),
-                ("slots", C.c_uint64), ("chunks_per_slot", C.c_uint64)]
+                ("slots", C.c_uint64), ("chunks_per_slot", C.c_uint64), ("chunks_skew", C.c_uint64)]
 
 
 def lorenz_launch_plan(key: Key, n: int, b0: int, b1: int) -> dict:
@@ -188,7 +188,7 @@ def lorenz_launch_plan(key: Key, n: int, b0: int, b1: int) -> dict:
     p = lorenz_plan()
     _check(lib().lorenz_launch_plan(C.byref(key.raw), n, b0, b1, C.byref(p)), "lorenz_launch_plan")
     return {"kind": ("wave", "balanced")[p.kind], "cta": p.cta, "grid": p.grid, "lanes": p.lanes,
-            "slots": p.slots, "chunks_per_slot": p.chunks_per_slot}
+            "slots": p.slots, "chunks_per_slot": p.chunks_per_slot, "chunks_skew": p.chunks_skew}
 
 
 def lorenz_num_blocks(key: Key, n: int) -> int:

@@ -115,10 +115,13 @@ def test_launch_plan_rules(L, monkeypatch):
     plan = lambda blocks: L.lorenz_launch_plan(key, blocks * 1024, 0, blocks)
     p = plan(65536)  # C3: 2,048 units, 3.46 warps per sub-partition in one wave
     assert p["kind"] == "balanced" and p["cta"] == 384 and p["grid"] == 148 and p["slots"] == 1776
-    assert p["chunks_per_slot"] == -(-2048 * 65 // 1776) >= 65
+    # skewed: 3 warp groups per CTA, the slots of group g hold 74 + g chunks (mean 75 = ceil(2048 x 65 / 1776))
+    assert p["chunks_per_slot"] == 74 and p["chunks_skew"] == 1
     assert plan(131072)["kind"] == "balanced" and plan(131072)["cta"] == 512  # C4 per rank at N = 8
-    assert plan(1 << 20)["kind"] == "wave"           # C4 at N = 1: 13.8 waves
-    assert plan(262144)["kind"] == "wave"            # C4 per rank at N = 4
+    assert plan(1 << 20)["kind"] == "balanced"       # C4 at N = 1 (RK4: every size from 2 warps/SMSP)
+    assert plan(262144)["kind"] == "balanced"        # C4 per rank at N = 4
+    eul = L.lorenz_keysetup(b"0123456789abcdef", mode=L.FAST, integrator=L.EULER)
+    assert L.lorenz_launch_plan(eul, 1 << 30, 0, 1 << 20)["kind"] == "wave"  # Euler: wave from 3 waves
     assert plan(75776)["kind"] == "wave"             # exactly 4 warps per sub-partition
     assert plan(37888)["kind"] == "wave"             # exactly 2 warps per sub-partition
     assert plan(1024)["kind"] == "wave" and plan(1024)["grid"] * plan(1024)["cta"] >= 1024  # C2
@@ -130,15 +133,16 @@ def test_launch_plan_rules(L, monkeypatch):
     monkeypatch.setenv("LORENZ_SCHED", "seg")
     monkeypatch.setenv("LORENZ_SEG_SLOTS", "3")
     p = plan(160)
-    assert p["kind"] == "balanced" and p["slots"] == 3 and p["chunks_per_slot"] == 109
+    assert p["kind"] == "balanced" and p["slots"] == 3 and p["chunks_per_slot"] == 109 and p["chunks_skew"] == 0
     with pytest.raises(L.LorenzError):
         L.lorenz_launch_plan(key, 1024, 0, 2)
 
 
 def test_launch_plan_mcnaughton_invariants(L, monkeypatch):
     """For every balanced plan: slots <= units (else a slot would hold less than one unit),
-    chunks_per_slot >= Q = (B+16)/16 (a cut unit's two pieces then never overlap in time),
-    slots * chunks_per_slot covers the U * Q chunk line, and the grid holds every slot."""
+    every slot holds >= Q = (B+16)/16 chunks (a cut unit's two pieces then never overlap in time;
+    skewed plans keep Q/8 more), the slots cover the U * Q chunk line without a spare slot's worth,
+    and the grid holds every slot."""
     monkeypatch.delenv("LORENZ_SCHED", raising=False)
     monkeypatch.delenv("LORENZ_SEG_SLOTS", raising=False)
     import random
@@ -158,6 +162,11 @@ def test_launch_plan_mcnaughton_invariants(L, monkeypatch):
                 continue
             units = -(-p["lanes"] // 32)
             assert 2 * 592 <= p["slots"] <= units
-            assert p["chunks_per_slot"] >= q
-            assert p["slots"] * p["chunks_per_slot"] >= units * q > p["slots"] * (p["chunks_per_slot"] - 1)
             assert p["grid"] == 148 and p["cta"] * p["grid"] // 32 >= p["slots"]
+            wpc = p["cta"] // 32
+            caps = ([p["chunks_per_slot"] + (w // 4) * p["chunks_skew"] for w in range(wpc)] * p["grid"])[:p["slots"]]
+            if p["chunks_skew"]:
+                assert p["slots"] == wpc * p["grid"]
+                assert p["chunks_per_slot"] >= q + q // 8  # slack: the pieces of a cut unit never meet
+            assert min(caps) >= q
+            assert sum(caps) >= units * q > sum(caps) - len(caps) - p["grid"] * wpc * p["chunks_skew"]
