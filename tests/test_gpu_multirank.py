@@ -22,19 +22,19 @@ def run(cmd, env):
     return lines
 
 
-@pytest.mark.parametrize("workload", ["c3", "c5"])
+@pytest.mark.parametrize("workload", ["c3", "c4", "c5"])
 def test_two_ranks_one_gpu_gloo(workload):
     env = dict(os.environ, LORENZ_DIST_BACKEND="gloo")
     args = ["bench.py", "--workload", workload, "--steps", "1", "--warmup", "1", "--no-cpu-baseline"]
     if workload == "c5":
         args += ["--c5-trials", "8"]
     two = run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
-               "--master-addr", "127.0.0.1", "--master-port", "29531" if workload == "c3" else "29532"]
+               "--master-addr", "127.0.0.1", "--master-port", {"c3": "29531", "c4": "29533", "c5": "29532"}[workload]]
               + args + ["--gpus", "2"], env)
     assert len(two) == 1, two  # rank 0 alone prints
     d2 = json.loads(two[0])
     assert d2["n_gpus"] == 2 and d2["value"] > 0 and d2["clocks"]["sm_mhz"] > 0
-    if workload == "c3":
+    if workload in ("c3", "c4"):  # c4: the driver's N = 2 slices (512 MiB each, balanced kernel)
         assert d2["validated"]["round_trip"] is True
         assert d2["e2e"]["matches_device_ct"] is True
         one = run([sys.executable] + args + ["--gpus", "1"], os.environ.copy())
