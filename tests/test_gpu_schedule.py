@@ -305,3 +305,33 @@ def test_seg_concurrent_launches_with_a_full_gpu_kernel(sched):
     for (pw, key, msg), (ct, tag) in zip(cases, out):
         want, want_tag = oracle.encrypt(pw, msg, oparams(key))
         assert np.array_equal(ct, want) and tag == want_tag
+
+
+@pytest.mark.parametrize("blocks,skew", [(40000, 8), (56000, 30), (65536, 60), (100000, 15), (140000, 120)])
+def test_seg_skewed_slots_equal_wave(sched, monkeypatch, blocks, skew):
+    """Skewed slot capacities (later warp groups of a CTA get more chunks) at default slot
+    layouts, including skews far above the tuned 8 per mille: ciphertext, tag and verdicts equal
+    the wave kernel's, and sampled blocks equal the oracle's."""
+    n = blocks * 1024 - 333
+    pw = inputs.password(seed=blocks)
+    msg = inputs.message(n, seed=skew)
+    key = L.lorenz_keysetup(pw, mode=L.FAST, n_it=3)
+    nb = key.num_blocks(n)
+    pt = torch.from_numpy(msg).to(DEV)
+    monkeypatch.setenv("LORENZ_SEG_SKEW", str(skew))
+    sched(mode="seg")
+    p = L.lorenz_launch_plan(key, n, 0, nb)
+    assert p["kind"] == "balanced"
+    ct_seg = torch.empty(key.ct_len(n), dtype=torch.uint8, device=DEV)
+    tag_seg = L.lorenz_encrypt(key, n, 0, nb, pt, ct_seg)
+    st, fb, _ = L.lorenz_verify(key, n, 0, nb, ct_seg)
+    assert (st, fb) == (L.OK, -1)
+    sched(mode="wave")
+    ct_wave = torch.empty_like(ct_seg)
+    assert L.lorenz_encrypt(key, n, 0, nb, pt, ct_wave) == tag_seg
+    assert torch.equal(ct_seg, ct_wave)
+    prm = oparams(key)
+    for b in [0, nb - 1, nb // 2]:
+        blk = msg[b * 1024:(b + 1) * 1024]
+        want = oracle.encrypt_block(pw, n, b, blk, prm)
+        assert np.array_equal(ct_seg[b * 1040:b * 1040 + len(want)].cpu().numpy(), want), f"block {b}"
