@@ -201,7 +201,7 @@ bool seg_plan(const lz::DevConst& C, uint32_t integrator, lz::SegPlan* P, int* c
     // SMs. RK4 keeps the balanced kernel at every larger size (1 GiB: 98.05 % against 97.9 %).
     if (w < 2) return false;
     if (integrator != LORENZ_RK4 && U > 3 * 16 * sms) return false;
-    // RK4-FMA: the wave kernel runs 20 warps per SM (5 x 128 threads, <= 102 registers), which
+    // RK4-FMA: the wave kernel runs 20 warps per SM (5 x 128 threads, <= 96 registers), which
     // its shorter dependent chains need; the balanced kernel's 12-16 reach ~85 %, so it only wins
     // while the wave kernel's single wave splits badly (C3: 85 % vs 78 %; 128 MiB: 84 % vs 90 %)
     if (integrator == LORENZ_RK4_FMA && U >= 24 * sms) return false;
@@ -216,7 +216,7 @@ bool seg_plan(const lz::DevConst& C, uint32_t integrator, lz::SegPlan* P, int* c
     const uint64_t v = std::strtoull(f, nullptr, 10);
     if (v) S = v;
   }
-  if (S > U) S = U;
+  if (S > U) S = U;  // S <= U gives Cq >= Q: a unit spans at most two slots (the kernel relies on it)
   P->units = U;
   P->q = (uint32_t)((C.B + 16 + 15) / 16);
   P->slots = (uint32_t)S;
