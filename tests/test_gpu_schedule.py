@@ -335,3 +335,36 @@ def test_seg_skewed_slots_equal_wave(sched, monkeypatch, blocks, skew):
         blk = msg[b * 1024:(b + 1) * 1024]
         want = oracle.encrypt_block(pw, n, b, blk, prm)
         assert np.array_equal(ct_seg[b * 1040:b * 1040 + len(want)].cpu().numpy(), want), f"block {b}"
+
+
+def test_seg_default_tamper_zero_fills_whole_slice(sched):
+    """At a size where the library itself picks the balanced kernel, a flipped byte (in a unit
+    the schedule cuts) is reported with its block by verify and decrypt; decrypt without
+    per-block verdicts zero-fills the whole slice, with them only the failing block."""
+    sched()
+    blocks = 70000
+    n = blocks * 1024
+    pw = inputs.password(seed=70)
+    msg = inputs.message(n, seed=70)
+    key = L.lorenz_keysetup(pw, mode=L.FAST, n_it=2)
+    p = L.lorenz_launch_plan(key, n, 0, blocks)
+    assert p["kind"] == "balanced"
+    ct, _ = run_all(key, msg)
+    # a block in the unit cut by the boundary between the first two positions of the chunk line
+    cut_unit = p["chunks_per_slot"] // 65
+    bad_block = 32 * cut_unit + 17
+    ct[bad_block * 1040 + 1000] ^= 1
+    st, fb, _ = L.lorenz_verify(key, n, 0, blocks, ct)
+    assert (st, fb) == (L.E_INTEGRITY, bad_block)
+    back = torch.full((n,), 9, dtype=torch.uint8, device=DEV)
+    st, fb = L.lorenz_decrypt(key, n, 0, blocks, ct, back)
+    assert (st, fb) == (L.E_INTEGRITY, bad_block)
+    assert int(back.count_nonzero()) == 0
+    ok = torch.zeros(blocks, dtype=torch.uint8, device=DEV)
+    st, fb = L.lorenz_decrypt(key, n, 0, blocks, ct, back, block_ok=ok)
+    assert (st, fb) == (L.E_INTEGRITY, bad_block)
+    assert int(ok.sum()) == blocks - 1 and int(ok[bad_block]) == 0
+    got = back.cpu().numpy()
+    assert not got[bad_block * 1024:(bad_block + 1) * 1024].any()
+    assert np.array_equal(got[:bad_block * 1024], msg[:bad_block * 1024])
+    assert np.array_equal(got[(bad_block + 1) * 1024:], msg[(bad_block + 1) * 1024:])
