@@ -301,6 +301,33 @@ def run_c5(a):
         return float(t.item())
     ms = mx(statistics.mean(step_ms))
     co, hi, lo = bt.results()
+
+    # e2e through the public calls a user makes for one C5 batch: the plaintexts H2D from pinned
+    # host memory, lorenz_encrypt_batch, the statistics calls, and the statistics D2H
+    e2e = None
+    if not a.no_e2e:
+        pts_pin = torch.from_numpy(bt.pts_h).pin_memory()
+
+        def e2e_step():
+            bt.pts.copy_(pts_pin, non_blocking=True)
+            bt.encrypt()
+            bt.statistics()
+            return bt.results()
+        for _ in range(2):
+            e2e_step()
+        times = []
+        for _ in range(a.steps):
+            torch.cuda.synchronize()
+            if dist_on:
+                dist.barrier()
+            t0 = time.perf_counter()
+            r = e2e_step()
+            times.append(time.perf_counter() - t0)
+        e2e_s = mx(statistics.mean(times))
+        e2e = {"value": round(world * 3 * T * n / e2e_s / 1e6, 3), "unit": "MB/s",
+               "h2d_bytes_per_step": int(pts_pin.numel()), "d2h_bytes_per_step": int(sum(x.nbytes for x in r)),
+               "api": "H2D + lorenz_encrypt_batch + lorenz_compare_spans / lorenz_histograms + D2H",
+               "ms_per_step": round(e2e_s * 1e3, 3)}
     pw_bits = co[:, 0, 0] / (8 * bt.ctl)
     ent = [sweep.entropy_bits(h) for h in hi]
     value = world * 3 * T * n / (ms / 1e3) / 1e6
@@ -324,7 +351,7 @@ def run_c5(a):
                                "locked_block_fraction": float((lo[:, :, 2] == B - sweep.LOCK_FROM).mean())},
             "gpu_launches": a.steps * (1 + 2 + 1 + -(-len(bt.lsb_spans) // 65535)),
             "clocks": clocks,
-            "e2e": None,
+            "e2e": e2e,
         }), flush=True)
     if dist_on:
         dist.barrier()
