@@ -251,7 +251,15 @@ lorenz_status lorenz_power_spectrum(const uint8_t* x, uint32_t H, uint32_t W, do
 /* ---- end to end from HOST buffers (the user-facing call of a file encryptor):
  * blocks [b0,b1) of an n-byte message; pt_host / ct_host are HOST pointers to the
  * slice starts (same slice convention as the device calls; [0, num_blocks) is the
- * whole message). Host->device copies, kernels and device->host copies are
+ * whole message).
+ * n_chunks = 0 (automatic) with both slices in page-locked memory mapped into the current
+ * device's address space (cudaHostAlloc / cudaMallocHost, torch pin_memory(),
+ * cudaHostRegister(..., cudaHostRegisterMapped)): DIRECT streaming — one chain launch reads
+ * the input and writes the output over PCIe itself (no device buffers; the transfers overlap
+ * the arithmetic window by window, so the call takes the kernel's time: 98.9 % of the device
+ * rate at 64 MiB, 99.98 % at 1 GiB, profiles/e2e_probe_r02.jsonl).
+ * Otherwise (pageable memory, or n_chunks > 0) the STAGED pipeline: host->device copies,
+ * kernels and device->host copies are
  * pipelined over `n_chunks` block-aligned chunks (0 -> automatic: first and last chunk the
  * smallest that keep 2 warps of 32 blocks per SM sub-partition, middle chunks <= 128 MiB, one
  * chunk below twice that minimum; n_chunks > 0: equal chunks) on the current device. Chunk

@@ -57,6 +57,53 @@ def loop_stats(ins):
     return best
 
 
+def back_edges(ins):
+    """(target, branch address) of every backward branch: the loops of the function."""
+    out = []
+    for addr, op, ln in ins:
+        if op.startswith("BRA"):
+            m = re.search(r"0x([0-9a-f]+)", ln.split("BRA", 1)[1])
+            if m and int(m.group(1), 16) < addr:
+                out.append((int(m.group(1), 16), addr))
+    return out
+
+
+def innermost_fp64_loops(ins, min_fp64=10):
+    """Opcode counts of every innermost loop (no other loop inside it) with at least `min_fp64`
+    DADD/DMUL/DFMA and no MUFU (a correctly rounded division's loop is not an integrator)."""
+    edges = back_edges(ins)
+    inner = [e for e in edges if not any(o != e and e[0] <= o[0] and o[1] <= e[1] for o in edges)]
+    out = []
+    for t, a in inner:
+        c = collections.Counter(o.split(".")[0] for ad, o, _ in ins if t <= ad <= a)
+        if c["DADD"] + c["DMUL"] + c["DFMA"] >= min_fp64 and not c["MUFU"]:
+            out.append({"DADD": c["DADD"], "DMUL": c["DMUL"], "DFMA": c["DFMA"],
+                        "other": sum(c.values()) - c["DADD"] - c["DMUL"] - c["DFMA"]})
+    return out
+
+
+CHAIN = re.compile(r"(lorenz_chain(?:_seg)?_kernel)ILi(\d)ELi(\d)ELi(\d+)E")
+
+
+def chain_kernel_loops(so):
+    """{(kernel, OP, INTEG, CTA): ([innermost FP64 loops], local-memory instructions)} for every
+    chain kernel instantiation in the library (cuobjdump -sass of those functions only)."""
+    names = subprocess.run(["cuobjdump", "-res-usage", so], capture_output=True, text=True, check=True).stdout
+    funs = sorted(set(re.findall(r"Function (_ZN2lz\w*lorenz_chain\w+):", names)))
+    sass = subprocess.run(["cuobjdump", "-sass", "-fun", ",".join(funs), so], capture_output=True, text=True,
+                          check=True).stdout
+    out = {}
+    for name, body in kernels(sass):
+        m = CHAIN.search(name)
+        if not m:
+            continue
+        ins = parse(body)
+        ops = collections.Counter(o.split(".")[0] for _, o, _ in ins)
+        out[(m.group(1), int(m.group(2)), int(m.group(3)), int(m.group(4)))] = (
+            innermost_fp64_loops(ins), ops["LDL"] + ops["STL"])
+    return out
+
+
 def main():
     so = sys.argv[1] if len(sys.argv) > 1 else "paper_1201_3114_b200/csrc/liblorenz.so"
     sass = subprocess.run(["cuobjdump", "-sass", so], capture_output=True, text=True, check=True).stdout
