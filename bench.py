@@ -88,6 +88,15 @@ def fp64_ops(n: int, B: int, b0: int, b1: int, n_it: int, integrator: str = "rk4
     return chars * (STEP_OPS[integrator] * n_it + OPS_PER_CHAR_EXTRA)
 
 
+def sm_max_mhz() -> float:
+    """The SM clock ceiling of the FP64 peak: MEASURED_PEAKS.json's sm_max_mhz (driver-written),
+    else the B200 maximum (/opt/skills/guides/B200_PROFILING.md)."""
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["sm_max_mhz"])
+    except (OSError, ValueError, KeyError):
+        return 1965.0
+
+
 def cores() -> int:
     try:
         return len(os.sched_getaffinity(0))
@@ -225,24 +234,63 @@ def run_reference(a):
 ORACLE_INTEG = {"rk4": 0, "euler": 1, "rk4fma": 2}  # oracle.RK4 / EULER / RK4_FMA
 
 
-def cpu_baseline(pw, n_it, B, n, target_s, integrator="rk4"):
+def lscpu_model() -> dict:
+    """CPU model as lscpu reports it (plus the core/socket counts), else /proc/cpuinfo's."""
+    out = {"model": cpu_model()}
+    try:
+        r = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10)
+        for ln in r.stdout.splitlines():
+            k, _, v = ln.partition(":")
+            k, v = k.strip(), v.strip()
+            if k in ("Model name", "CPU(s)", "Socket(s)", "Thread(s) per core", "Hypervisor vendor", "CPU max MHz",
+                     "L3"):
+                out[k] = v
+    except (OSError, subprocess.SubprocessError):
+        pass
+    return out
+
+
+def cpu_baseline(pw, n_it, B, msg, target_s, integrator="rk4", gpu_ct=None, ranges=16):
+    """The oracle as it stands on this host's cores, on a bounded sample of the same message:
+    `ranges` contiguous block ranges spread evenly over it (about target_s of CPU time on all
+    threads), plus a single-thread rate on a smaller sample. The sample's ciphertext is compared
+    with the GPU's ciphertext of the same blocks (gpu_ct: the device tensor of the whole message)."""
     import oracle
-    from paper_1201_3114_b200 import inputs
+    n = len(msg)
+    nb = -(-n // B)
     prm = oracle.params(mode=oracle.FAST, n_it=n_it, block_size=B, integrator=ORACLE_INTEG[integrator])
     threads = cores()
     probe = max(threads, 8)
-    msg = inputs.message(probe * B)
     t0 = time.perf_counter()
     oracle.encrypt(pw, msg, prm, b0=0, b1=probe, threads=threads)
     per_block = (time.perf_counter() - t0) / probe
-    S = int(max(probe, min(target_s / per_block, n // B)))
-    msg = inputs.message(S * B)
+    per = max(threads, int(min(target_s / per_block, nb) // ranges))
+    starts = sorted({min(nb - per, (nb * i) // ranges) for i in range(ranges)})
+    sec, ok, blocks = 0.0, True, 0
+    for b0 in starts:
+        b1 = b0 + per
+        t0 = time.perf_counter()
+        ct, _ = oracle.encrypt(pw, msg, prm, b0=b0, b1=b1, threads=threads)
+        sec += time.perf_counter() - t0
+        blocks += b1 - b0
+        if gpu_ct is not None:
+            lo, hi = b0 * (B + 16), min(b1 * (B + 16), len(ct))
+            ok = ok and bool(np.array_equal(gpu_ct[lo:hi].cpu().numpy(), ct[lo:hi]))
+    # one thread: the oracle's per-core rate (SURVEY.md §8(d) "single-core MB/s")
+    s1 = max(2, int(3.0 / per_block / threads))
     t0 = time.perf_counter()
-    oracle.encrypt(pw, msg, prm, b0=0, b1=S, threads=threads)
-    sec = time.perf_counter() - t0
-    return {"value": round(S * B / sec / 1e6, 4), "unit": "MB/s", "cores": threads, "kind": "oracle",
-            "sample": f"blocks [0,{S}) of the same message ({S * B} bytes), all {threads} threads, "
-                      f"{sec:.1f} s", "cpu": cpu_model()}
+    oracle.encrypt(pw, msg, prm, b0=0, b1=s1, threads=1)
+    one = time.perf_counter() - t0
+    cpu = lscpu_model()
+    res = {"value": round(blocks * B / sec / 1e6, 4), "unit": "MB/s", "cores": threads, "kind": "oracle",
+           "sample": f"{len(starts)} ranges of {per} blocks spread evenly over the same message "
+                     f"({blocks * B} bytes), all {threads} threads, {sec:.1f} s",
+           "single_core_mbps": round(s1 * B / one / 1e6, 4), "single_core_sample": f"blocks [0,{s1}), 1 thread",
+           "cpu": cpu.get("Model name", cpu["model"]), "lscpu": cpu}
+    val = None
+    if gpu_ct is not None:
+        val = {"oracle_blocks": blocks, "oracle_ranges": len(starts), "oracle_ok": ok}
+    return res, val
 
 
 # ---------------------------------------------------------------- C5 sweep arm
@@ -333,7 +381,7 @@ def run_c5(a):
     value = world * 3 * T * n / (ms / 1e3) / 1e6
     ops = 3 * T * fp64_ops(n, B, 0, n // B, a.n_it)
     achieved = ops / (statistics.mean(enc_ms) / 1e3) / 1e12
-    peak = SMS * FP64_LANES_PER_SM * 1965.0 * 1e6 / 1e12
+    peak = SMS * FP64_LANES_PER_SM * sm_max_mhz() * 1e6 / 1e12
     if rank == 0:
         print(json.dumps({
             "metric": METRIC, "value": round(value, 3), "unit": "MB/s", "n_gpus": world, "steps": a.steps,
@@ -359,6 +407,16 @@ def run_c5(a):
 
 
 # ---------------------------------------------------------------- our arm
+def golden_tag(workload_name: str, n_it: int, integrator: str):
+    """The oracle's digest of this workload (tests/golden/oracle_tags.json, written by
+    tools/oracle_tags.py from oracle/ alone), or None if not recorded."""
+    try:
+        g = json.load(open(os.path.join(ROOT, "tests", "golden", "oracle_tags.json")))
+    except (OSError, ValueError):
+        return None
+    return g.get(f"{workload_name}/n_it={n_it}/{integrator}")
+
+
 def main():
     a = parse()
     if a.impl == "reference":
@@ -381,6 +439,7 @@ def main():
     torch.cuda.set_device(dev)
     if dist_on:
         init_dist(dev)
+        world = dist.get_world_size()  # the rank count the communicator saw
     name, n = workload(a.workload)
     B = 1024
     pw = inputs.password()
@@ -414,6 +473,12 @@ def main():
             mid.record(stream)
         return D.min_combine(eng.first_bad()) if dist_on else eng.first_bad()
 
+    def step_verify(mid=None):
+        eng.verify(b0, b1, ct)
+        if mid is not None:
+            mid.record(stream)
+        return D.min_combine(eng.first_bad()) if dist_on else eng.first_bad()
+
     def timed(fn, K):
         """K steps; L2 flushed (write > L2) between steps, outside the events.
         Returns (step ms incl. the combine collective, kernel-only ms) per step."""
@@ -435,13 +500,16 @@ def main():
     with ClockSampler(gpu_id) as clk:
         enc_ms, enc_kernel_ms = timed(step_encrypt, a.steps)
     clocks = clk.summary()
-    tag = step_encrypt().cpu().numpy().tobytes()
+    my_tag = eng.encrypt(b0, b1, pt, ct).cpu().numpy().tobytes()  # this rank's slice digest
+    tag = step_encrypt().cpu().numpy().tobytes()                  # combined over the ranks
 
     for _ in range(min(a.warmup, 1)):
         step_decrypt()
     dec_ms, _ = timed(step_decrypt, a.steps)
     fb = int(step_decrypt().item())
     ok = fb == D.NO_BAD and torch.equal(back, pt)
+    ver_ms, _ = timed(step_verify, max(1, a.steps // 2))
+    vfb = int(step_verify().item())
 
     def max_over_ranks(x: float) -> float:
         if not dist_on:
@@ -452,7 +520,8 @@ def main():
 
     enc_sum = max_over_ranks(sum(enc_ms))
     dec_sum = max_over_ranks(sum(dec_ms))
-    oks = max_over_ranks(0.0 if ok else 1.0) == 0.0
+    ver_mean = max_over_ranks(statistics.mean(ver_ms))
+    oks = max_over_ranks(0.0 if (ok and vfb == D.NO_BAD) else 1.0) == 0.0
     ms_step = enc_sum / a.steps
     value = n / (ms_step / 1e3) / 1e6
     dec_value = n / (dec_sum / a.steps / 1e3) / 1e6
@@ -462,10 +531,7 @@ def main():
     ops = fp64_ops(n, B, b0, b1, a.n_it, a.integrator)
     kern_s = statistics.mean(enc_kernel_ms) / 1e3  # result init + chain kernel on the launching stream
     achieved = ops / kern_s / 1e12
-    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
-        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
-    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
-    peak = SMS * FP64_LANES_PER_SM * sm_max * 1e6 / 1e12
+    peak = SMS * FP64_LANES_PER_SM * sm_max_mhz() * 1e6 / 1e12
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_chain_kernel.json")
     if os.path.exists(tpath) and a.workload == "c4" and a.integrator == "rk4" and a.n_it == 100:
@@ -480,33 +546,70 @@ def main():
         except (ValueError, OSError):
             traffic = None
 
-    # e2e through the host-buffer C-ABI call (pinned host slices)
-    e2e = None
+    # per-rank evidence for the driver's scaling runs: every rank's slice, kernel time and digest
+    mine = {"rank": rank, "blocks": [b0, b1], "kernel_ms_mean": round(statistics.mean(enc_kernel_ms), 3),
+            "step_ms_mean": round(statistics.mean(enc_ms), 3), "tag": my_tag.hex(), "device": str(dev),
+            "gpu": gpu_id}
+    if dist_on:
+        ranks = [None] * world
+        dist.all_gather_object(ranks, mine)
+    else:
+        ranks = [mine]
+
+    # e2e through the host-buffer C-ABI calls (pinned host slices: direct PCIe streaming)
+    e2e = dec_e2e = None
     if not a.no_e2e:
         pt_h = torch.from_numpy(msg).pin_memory()
         ct_h = torch.empty(sl.ct_bytes, dtype=torch.uint8).pin_memory()
+        back_h = torch.empty(sl.pt_bytes, dtype=torch.uint8).pin_memory()
         t_dev = torch.empty(16, dtype=torch.uint8, device=dev)
-        for _ in range(2):  # warm the pool, the streams and the host path
-            L.lorenz_encrypt_host(key, n, b0, b1, pt_h, ct_h)
-        times = []
-        for _ in range(a.steps):
-            barrier()
-            t0 = time.perf_counter()
+        fb_dev = torch.empty(1, dtype=torch.int64, device=dev)
+
+        def host_enc():
             t = L.lorenz_encrypt_host(key, n, b0, b1, pt_h, ct_h)
             if dist_on:
                 t_dev.copy_(torch.frombuffer(bytearray(t), dtype=torch.uint8))
                 D.xor_combine(t_dev).cpu()
-            times.append(time.perf_counter() - t0)
-        e2e_s = max_over_ranks(statistics.mean(times))
-        e2e = {"value": round(n / e2e_s / 1e6, 3), "unit": "MB/s", "h2d_bytes_per_step": sl.pt_bytes,
-               "d2h_bytes_per_step": sl.ct_bytes + 16, "api": "lorenz_encrypt_host (pinned host buffers)",
-               "ms_per_step": round(e2e_s * 1e3, 3), "matches_device_ct": bool(torch.equal(ct_h.to(dev), ct))}
 
-    cpu = None
+        def host_dec():
+            st, f = L.lorenz_decrypt_host(key, n, b0, b1, ct_h, back_h)
+            if dist_on:
+                fb_dev.fill_(D.NO_BAD if f < 0 else f)
+                D.min_combine(fb_dev).cpu()
+
+        def e2e_time(fn):
+            for _ in range(2):  # warm the pool, the streams and the host path
+                fn()
+            times = []
+            for _ in range(a.steps):
+                barrier()
+                t0 = time.perf_counter()
+                fn()
+                times.append(time.perf_counter() - t0)
+            return max_over_ranks(statistics.mean(times))
+        e2e_s = e2e_time(host_enc)
+        matches = bool(torch.equal(ct_h.to(dev), ct))
+        dec_s = e2e_time(host_dec)
+        e2e = {"value": round(n / e2e_s / 1e6, 3), "unit": "MB/s", "h2d_bytes_per_step": sl.pt_bytes,
+               "d2h_bytes_per_step": sl.ct_bytes + 16,
+               "api": "lorenz_encrypt_host (pinned host buffers: the kernel streams them over PCIe)",
+               "ms_per_step": round(e2e_s * 1e3, 3), "frac_of_device": round(ms_step / (e2e_s * 1e3), 4),
+               "matches_device_ct": matches}
+        dec_e2e = {"value": round(n / dec_s / 1e6, 3), "unit": "MB/s", "h2d_bytes_per_step": sl.ct_bytes,
+                   "d2h_bytes_per_step": sl.pt_bytes + 8, "api": "lorenz_decrypt_host (pinned host buffers)",
+                   "ms_per_step": round(dec_s * 1e3, 3), "round_trip": bool(torch.equal(back_h, pt_h))}
+
+    cpu = val = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
-        cpu = cpu_baseline(pw, a.n_it, B, n, a.cpu_seconds, a.integrator)
+        cpu, val = cpu_baseline(pw, a.n_it, B, msg, a.cpu_seconds, a.integrator, gpu_ct=ct)
 
     if rank == 0:
+        want_tag = golden_tag(a.workload, a.n_it, a.integrator)
+        kms = [r["kernel_ms_mean"] for r in ranks]
+        validated = {"round_trip": oks, "verify_ok": vfb == D.NO_BAD, "tag_xor": tag.hex(),
+                     "oracle_tag_xor": want_tag, "tag_matches_oracle": (tag.hex() == want_tag) if want_tag else None}
+        if val:
+            validated.update(val)
         out = {
             "metric": METRIC, "value": round(value, 3), "unit": "MB/s", "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": True, "scaling": "strong",
@@ -516,6 +619,7 @@ def main():
                        "parallelism": f"blocks{world}",
                        "l2": "flushed between timed steps (2x126 MB write) and inputs > L2"},
             "decrypt": {"value": round(dec_value, 3), "unit": "MB/s", "ms_per_step": round(dec_sum / a.steps, 3)},
+            "verify": {"value": round(n / ver_mean / 1e3, 3), "unit": "MB/s", "ms_per_step": round(ver_mean, 3)},
             "roofline": {"bound": "alu", "achieved": round(achieved, 4), "peak": round(peak, 4), "unit": "TFLOP/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic,
                          "kernel": kernel_label(plan, a.integrator), "schedule": plan,
@@ -523,8 +627,11 @@ def main():
                          "hbm_gbs": round((sl.pt_bytes + sl.ct_bytes) / kern_s / 1e9, 3),
                          "kernel_ms": round(kern_s * 1e3, 3)},
             "fp64_pipe_pct": round(100 * achieved / peak, 2),
-            "validated": {"round_trip": oks, "tag_xor": tag.hex()},
+            "validated": validated,
+            "ranks": {"world_size": world, "backend": dist.get_backend() if dist_on else None,
+                      "kernel_ms_max": max(kms), "kernel_ms_min": min(kms), "per_rank": ranks},
             "e2e": e2e,
+            "decrypt_e2e": dec_e2e,
             "gpu_launches": 2 * a.steps,
             "clocks": clocks,
         }

@@ -117,8 +117,8 @@ lorenz_status lorenz_pt_len(const lorenz_key* k, uint64_t ct_len, uint64_t* n_ou
  * lanes' 32-block units, (B+16)/16 chunks each, are dealt to `slots` resident warps,
  * `chunks_per_slot` chunks each, a unit cut by a slot boundary handing its chain states
  * from one warp to the next. Chooses exactly as the encrypt/decrypt/verify calls do
- * (LORENZ_SCHED / LORENZ_SEG_SLOTS overrides included). LORENZ_E_ARG on a NULL or bad
- * key/out or an out-of-range block range. */
+ * (lorenz_set_tuning overrides included). LORENZ_E_ARG on a NULL or bad key/out or an
+ * out-of-range block range. */
 typedef struct {
   uint32_t kind;            /* 0 wave, 1 balanced                                     */
   uint32_t cta;             /* threads per CTA                                        */
@@ -133,6 +133,25 @@ typedef struct {
 lorenz_status lorenz_launch_plan(const lorenz_key* k, uint64_t n, uint64_t b0, uint64_t b1,
                                  lorenz_plan* out);
 const char* lorenz_status_string(lorenz_status s);
+
+/* Tuning / test overrides of the chain kernels' launch plan (process-wide; normal use never
+ * needs them, and the library reads no environment variables). Fields:
+ *   schedule   0 automatic (the rule of DESIGN.md §4), 1 force the wave kernel, 2 force the
+ *              balanced kernel (any size, RK4 / Euler / RK4-FMA);
+ *   seg_slots  balanced kernel: warp slots (0 = SMs x warps per CTA; clamped to the 32-block
+ *              units, so every unit spans at most two slots);
+ *   seg_skew   balanced kernel: slot skew per warp group in per mille of a slot (-1 = the
+ *              default 8, 0 = equal slots);
+ *   cta        wave kernel: threads per CTA (0 = automatic; 128, 256 or 512).
+ * t = NULL restores every default. Thread-safe; applies to plans made after the call.
+ * LORENZ_E_ARG for a field out of range (nothing is changed then). */
+typedef struct {
+  uint32_t schedule;
+  uint32_t seg_slots;
+  int32_t seg_skew;
+  uint32_t cta;
+} lorenz_tuning;
+lorenz_status lorenz_set_tuning(const lorenz_tuning* t);
 const char* lorenz_last_error(void);
 int lorenz_abi_version(void);
 
@@ -165,7 +184,8 @@ lorenz_status lorenz_verify(const lorenz_key* k, uint64_t n, uint64_t b0, uint64
                             void* cuda_stream);
 
 /* ---- asynchronous forms: enqueue and return; results accumulate into `res`
- * (device, see lorenz_result). Safe inside CUDA graph capture. ---- */
+ * (device, see lorenz_result; 16-byte aligned, else LORENZ_E_ARG: the kernels update it with
+ * 64-bit atomics). Safe inside CUDA graph capture. ---- */
 lorenz_status lorenz_result_init_async(lorenz_result* res, void* cuda_stream);
 lorenz_status lorenz_encrypt_async(const lorenz_key* k, uint64_t n, uint64_t b0, uint64_t b1,
                                    const uint8_t* pt, uint8_t* ct, lorenz_result* res,
@@ -179,7 +199,8 @@ lorenz_status lorenz_verify_async(const lorenz_key* k, uint64_t n, uint64_t b0, 
 /* ---- batch (C5 sweeps): S independent messages of equal length n, one key each
  * (all keys must share mode/n_it/dt/B/integrator, else LORENZ_E_ARG). keys: HOST
  * array of S keys. Message s is at pts + s*n, its ciphertext at cts + s*ct_len(n),
- * its tag XOR at tags + 16*s (all DEVICE). One launch, lane = (message, block). */
+ * its tag XOR at tags + 16*s (all DEVICE; tags 16-byte aligned, else LORENZ_E_ARG).
+ * One launch, lane = (message, block). */
 lorenz_status lorenz_encrypt_batch(const lorenz_key* keys, uint32_t S, uint64_t n,
                                    const uint8_t* pts, uint8_t* cts, uint8_t* tags,
                                    void* cuda_stream);

@@ -8,10 +8,12 @@
 #include <nvtx3/nvToolsExt.h>  // header-only; ranges are no-ops unless a profiler attaches
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <utility>
 #include <vector>
@@ -140,14 +142,31 @@ lz::DevConst make_const(const KeyImpl* K, uint64_t n, uint64_t b0, uint64_t lane
   return C;
 }
 
+// SM count of the current device, cached per device (148 without a device).
 int sm_count() {
-  static int n = 0;
+  static std::atomic<int> cache[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) {
+    cudaGetLastError();
+    return 148;
+  }
+  int n = cache[dev].load(std::memory_order_relaxed);
   if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) {
+      cudaGetLastError();
+      n = 148;
+    }
+    cache[dev].store(n, std::memory_order_relaxed);
   }
   return n;
+}
+
+// lorenz_set_tuning's overrides (process-wide); launch plans read a snapshot
+std::mutex g_tuning_mu;
+lorenz_tuning g_tuning = {0, 0, -1, 0};
+lorenz_tuning tuning() {
+  std::lock_guard<std::mutex> lk(g_tuning_mu);
+  return g_tuning;
 }
 
 // CTA size for a launch of `lanes` chains (16 resident warps per SM either way). The kernel
@@ -157,10 +176,7 @@ int sm_count() {
 // 16 MiB to 1 GiB: the rule picked the faster size at every one).
 int chain_cta(uint64_t lanes, uint32_t integrator) {
   if (integrator == LORENZ_RK4_FMA) return 128;  // 5 CTAs/SM of 128 (see min_ctas)
-  if (const char* f = std::getenv("LORENZ_CTA")) {  // tuning override: 128 | 256 | 512
-    const int v = std::atoi(f);
-    if (v == 128 || v == 256 || v == 512) return v;
-  }
+  if (const uint32_t v = tuning().cta) return (int)v;  // lorenz_set_tuning: 128 | 256 | 512
   const uint64_t warps = (lanes + 31) / 32, sms = (uint64_t)sm_count();
   const uint64_t c128 = (warps + 3) / 4, c256 = (warps + 7) / 8;  // CTAs of 4 / 8 warps
   const uint64_t l128 = 4 * ((c128 + sms - 1) / sms), l256 = 8 * ((c256 + sms - 1) / sms);
@@ -175,7 +191,6 @@ cudaError_t launch_chain_cta(const lz::DevConst& C, const lz::DevKey& K, const l
   return cudaGetLastError();
 }
 
-void keep_pool_cached();
 
 // Balanced schedule (lz::lorenz_chain_seg_kernel, lorenz_device.cuh) for chain launches
 // with two or more warps of chains per SM sub-partition (exceptions below): one CTA of 128 w
@@ -185,14 +200,13 @@ void keep_pool_cached();
 // the warp schedulers favour the older of two co-resident CTAs (tools/seg_trace.py: with
 // 2 x 256 threads per SM the second CTA's warps ran at half rate until the first finished, and
 // slots cut across the two classes waited), while the warps of one CTA keep within ~3 %.
-// Overrides for tests and tuning: LORENZ_SCHED=wave|seg, LORENZ_SEG_SLOTS=S (clamped to U),
-// LORENZ_SEG_SKEW=per mille (0: equal slots).
+// Overrides for tests and tuning: lorenz_set_tuning (schedule, slots S clamped to U, skew).
 bool seg_plan(const lz::DevConst& C, uint32_t integrator, lz::SegPlan* P, int* cta) {
   if (integrator > LORENZ_RK4_FMA) return false;
-  const char* sched = std::getenv("LORENZ_SCHED");
-  if (sched && std::strcmp(sched, "wave") == 0) return false;
+  const lorenz_tuning T = tuning();
+  if (T.schedule == 1) return false;
   const uint64_t U = (C.lanes + 31) / 32, sms = (uint64_t)sm_count();
-  const bool forced = sched && std::strcmp(sched, "seg") == 0;
+  const bool forced = T.schedule == 2;
   uint64_t w = std::min<uint64_t>(4, U / (4 * sms));
   if (!forced) {
     // The wave kernel wins (tools/tune.py) in one wave whose warps split evenly
@@ -212,10 +226,7 @@ bool seg_plan(const lz::DevConst& C, uint32_t integrator, lz::SegPlan* P, int* c
   }
   if (w < 2) w = 2;
   uint64_t S = 4 * w * sms;
-  if (const char* f = std::getenv("LORENZ_SEG_SLOTS")) {
-    const uint64_t v = std::strtoull(f, nullptr, 10);
-    if (v) S = v;
-  }
+  if (T.seg_slots) S = T.seg_slots;
   if (S > U) S = U;  // S <= U gives Cq >= Q: a unit spans at most two slots (the kernel relies on it)
   P->units = U;
   P->q = (uint32_t)((C.B + 16 + 15) / 16);
@@ -232,8 +243,7 @@ bool seg_plan(const lz::DevConst& C, uint32_t integrator, lz::SegPlan* P, int* c
   // and only while every slot keeps >= Q/8 chunks of slack over a unit (the two pieces of a
   // cut unit must not meet: with no slack, 1,184 units over 1,184 skewed slots ran at 61 %).
   const uint64_t wpc = 4 * w, G = sms;
-  uint64_t skew = 8;
-  if (const char* f = std::getenv("LORENZ_SEG_SKEW")) skew = std::strtoull(f, nullptr, 10);
+  const uint64_t skew = T.seg_skew < 0 ? 8 : (uint64_t)T.seg_skew;
   if (skew && S == G * wpc) {
     const uint64_t UQ = U * P->q, ng = wpc / 4;
     const uint64_t dq = (UQ / S * skew + 500) / 1000;
@@ -258,7 +268,6 @@ cudaError_t launch_chain(const lz::DevConst& C, const lz::DevKey& K, const lz::D
   lz::SegPlan P;
   int scta = 0;
   if (seg_plan(C, integrator, &P, &scta)) {
-    keep_pool_cached();
     const cudaError_t e = lz::launch_seg_op<OP>(C, P, scta, integrator, K, Kb, in, out, res, tags, block_ok, st);
     if (e != cudaErrorNotReady) return e;  // cudaErrorNotReady: scratch allocation failed, fall through
   }
@@ -305,24 +314,8 @@ lorenz_status finish_sync(lorenz_result* d_res, cudaStream_t st, lorenz_result* 
   return LORENZ_OK;
 }
 
-// The library's small per-call buffers come from the device's stream-ordered pool. With the
-// default release threshold (0) every synchronisation hands freed pages back to the driver
-// and the next call maps them again; keep them cached instead (once per device).
-void keep_pool_cached() {
-  static bool done[64] = {};
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64 || done[dev]) return;
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-    uint64_t thr = ~0ULL;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-  }
-  done[dev] = true;
-}
-
 lorenz_status alloc_result(lorenz_result** d_res, cudaStream_t st) {
-  keep_pool_cached();
-  if (!cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(d_res), sizeof(lorenz_result), st), "cudaMallocAsync"))
+  if (!cuda_ok(lz::lib_malloc_async(reinterpret_cast<void**>(d_res), sizeof(lorenz_result), st), "cudaMallocAsync"))
     return LORENZ_E_CUDA;
   lz::result_init_kernel<<<1, 32, 0, st>>>(*d_res);
   return cuda_ok(cudaGetLastError(), "result_init") ? LORENZ_OK : LORENZ_E_CUDA;
@@ -332,6 +325,37 @@ lorenz_status alloc_result(lorenz_result** d_res, cudaStream_t st) {
 
 namespace lz {
 void set_last_error(const std::string& s) { g_err = s; }  // shared with lorenz_io.cu
+
+// The library's own stream-ordered pool, one per device, created on first use. Per-call scratch
+// (result slots, key arrays, hand-over state, FFT workspaces, staged host-path buffers) comes
+// from it; its release threshold keeps up to kPoolKeep bytes mapped across synchronisations so
+// repeated calls do not remap pages, and everything above that goes back to the driver at the
+// next synchronisation. The device's default pool and its policy are left alone.
+constexpr uint64_t kPoolKeep = 256ull << 20;
+cudaError_t lib_malloc_async(void** p, size_t bytes, cudaStream_t st) {
+  static std::mutex mu;
+  static cudaMemPool_t pools[64] = {};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= 64) return cudaMallocAsync(p, bytes, st);
+  cudaMemPool_t pool;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (!pools[dev]) {
+      cudaMemPoolProps props;
+      std::memset(&props, 0, sizeof props);
+      props.allocType = cudaMemAllocationTypePinned;
+      props.location.type = cudaMemLocationTypeDevice;
+      props.location.id = dev;
+      if ((e = cudaMemPoolCreate(&pools[dev], &props)) != cudaSuccess) return e;
+      uint64_t keep = kPoolKeep;
+      cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    pool = pools[dev];
+  }
+  return cudaMallocFromPoolAsync(p, bytes, pool, st);
+}
 }  // namespace lz
 
 // ======================================================================== C ABI
@@ -409,6 +433,19 @@ lorenz_status lorenz_keysetup(const uint8_t* pw, size_t pw_len, const lorenz_par
   return LORENZ_OK;
 }
 
+lorenz_status lorenz_set_tuning(const lorenz_tuning* t) {
+  lorenz_tuning v = {0, 0, -1, 0};
+  if (t) {
+    if (t->schedule > 2 || t->seg_skew < -1 || t->seg_skew > 100 ||
+        (t->cta && t->cta != 128 && t->cta != 256 && t->cta != 512))
+      return LORENZ_E_ARG;
+    v = *t;
+  }
+  std::lock_guard<std::mutex> lk(g_tuning_mu);
+  g_tuning = v;
+  return LORENZ_OK;
+}
+
 lorenz_status lorenz_key_params(const lorenz_key* k, lorenz_params* out) {
   const KeyImpl* K = impl(k);
   if (!K || !out) return LORENZ_E_ARG;
@@ -473,7 +510,7 @@ lorenz_status lorenz_encrypt_async(const lorenz_key* k, uint64_t n, uint64_t b0,
                                    const uint8_t* pt, uint8_t* ct, lorenz_result* res, void* stream) {
   Trace tr("lorenz_encrypt");
   const KeyImpl* K = impl(k);
-  if (!K || !res) return LORENZ_E_ARG;
+  if (!K || !res || !aligned16(res)) return LORENZ_E_ARG;  // 64-bit atomics on res
   uint64_t ptb = 0, ctb = 0;
   if (b0 < b1) slice_bytes(K, n, b0, b1, &ptb, &ctb);
   lorenz_status s = check_range(K, n, b0, b1, pt, ptb, ct, ctb);
@@ -490,7 +527,7 @@ lorenz_status lorenz_decrypt_async(const lorenz_key* k, uint64_t n, uint64_t b0,
                                    void* stream) {
   Trace tr("lorenz_decrypt");
   const KeyImpl* K = impl(k);
-  if (!K || !res) return LORENZ_E_ARG;
+  if (!K || !res || !aligned16(res)) return LORENZ_E_ARG;  // 64-bit atomics on res
   uint64_t ptb = 0, ctb = 0;
   if (b0 < b1) slice_bytes(K, n, b0, b1, &ptb, &ctb);
   lorenz_status s = check_range(K, n, b0, b1, ct, ctb, pt, ptb);
@@ -512,7 +549,7 @@ lorenz_status lorenz_verify_async(const lorenz_key* k, uint64_t n, uint64_t b0, 
                                   lorenz_result* res, void* stream) {
   Trace tr("lorenz_verify");
   const KeyImpl* K = impl(k);
-  if (!K || !res) return LORENZ_E_ARG;
+  if (!K || !res || !aligned16(res)) return LORENZ_E_ARG;  // 64-bit atomics on res
   uint64_t ptb = 0, ctb = 0;
   if (b0 < b1) slice_bytes(K, n, b0, b1, &ptb, &ctb);
   lorenz_status s = check_range(K, n, b0, b1, ct, ctb, nullptr, 0);
@@ -598,7 +635,8 @@ lorenz_status lorenz_encrypt_batch(const lorenz_key* keys, uint32_t S, uint64_t 
   }
   const uint64_t nb = nblocks(K0, n), ctl = n + 16 * nb;
   if (K0->prm.mode == LORENZ_FAST && nb > (1ULL << 32)) return LORENZ_E_ARG;
-  if ((n && (!pts || !aligned16(pts) || n % 16)) || !cts || !aligned16(cts) || !tags) return LORENZ_E_ARG;
+  if ((n && (!pts || !aligned16(pts) || n % 16)) || !cts || !aligned16(cts) || !tags || !aligned16(tags))
+    return LORENZ_E_ARG;
   if (overlap(pts, n * S, cts, ctl * S)) return LORENZ_E_ARG;
   cudaStream_t st = (cudaStream_t)stream;
   lz::DevKey* d_keys = nullptr;
@@ -607,7 +645,7 @@ lorenz_status lorenz_encrypt_batch(const lorenz_key* keys, uint32_t S, uint64_t 
   lorenz_status ret = LORENZ_OK;
   lorenz_result* d_res = nullptr;
   do {
-    if (!cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&d_keys), sizeof(lz::DevKey) * S, st), "alloc keys")) {
+    if (!cuda_ok(lz::lib_malloc_async(reinterpret_cast<void**>(&d_keys), sizeof(lz::DevKey) * S, st), "alloc keys")) {
       ret = LORENZ_E_CUDA; break;
     }
     if (!cuda_ok(cudaMemcpyAsync(d_keys, h_keys.data(), sizeof(lz::DevKey) * S, cudaMemcpyHostToDevice, st),
@@ -646,7 +684,7 @@ lorenz_status ragged(const lorenz_key* keys, uint32_t count, const uint64_t* n, 
                      const uint64_t* out_off, const uint8_t* in, uint8_t* out, uint8_t* tags, int64_t* first_bad,
                      bool decrypt, cudaStream_t st) {
   if (!keys || count == 0 || count > (1u << 30) || !n || !in_off || !out_off || !in || !out || !tags ||
-      !aligned16(in) || !aligned16(out) || (decrypt && !first_bad))
+      !aligned16(in) || !aligned16(out) || !aligned16(tags) || (decrypt && !first_bad))
     return LORENZ_E_ARG;
   const KeyImpl* K0 = impl(&keys[0]);
   if (!K0 || K0->prm.mode != LORENZ_FAST) return LORENZ_E_ARG;
@@ -673,25 +711,32 @@ lorenz_status ragged(const lorenz_key* keys, uint32_t count, const uint64_t* n, 
     out_end = std::max(out_end, out_off[s] + ob);
     outs[s] = {out_off[s], out_off[s] + ob};
   }
+  // non-empty output ranges must be disjoint: sorted by start, each starts at or after the
+  // furthest end so far (an empty range in between must not hide an overlap)
+  outs.erase(std::remove_if(outs.begin(), outs.end(), [](const std::pair<uint64_t, uint64_t>& r) {
+               return r.second <= r.first;
+             }), outs.end());
   std::sort(outs.begin(), outs.end());
-  for (uint32_t s = 1; s < count; ++s)
-    if (outs[s].first < outs[s - 1].second && outs[s].second > outs[s].first) {
+  uint64_t max_end = 0;
+  for (size_t s = 0; s < outs.size(); ++s) {
+    if (s && outs[s].first < max_end) {
       g_err = "ragged batch: output ranges overlap";
       return LORENZ_E_ARG;
     }
+    max_end = std::max(max_end, outs[s].second);
+  }
   if (overlap(in, in_end, out, out_end)) return LORENZ_E_ARG;
   const uint64_t lanes = blk[count];
   std::vector<lz::DevKey> h_keys(count);
   for (uint32_t s = 0; s < count; ++s) h_keys[s] = make_devkey(impl(&keys[s]));
-  keep_pool_cached();
   lz::DevKey* d_keys = nullptr;
   uint64_t* d_tab = nullptr;  // blk | len | in | out | bad
   lorenz_result* d_res = nullptr;
   lorenz_status ret = LORENZ_OK;
   std::vector<uint64_t> bad(count, ~0ULL);
   do {
-    if (!cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&d_keys), sizeof(lz::DevKey) * count, st), "alloc") ||
-        !cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&d_tab), 8 * (5ull * count + 1), st), "alloc")) {
+    if (!cuda_ok(lz::lib_malloc_async(reinterpret_cast<void**>(&d_keys), sizeof(lz::DevKey) * count, st), "alloc") ||
+        !cuda_ok(lz::lib_malloc_async(reinterpret_cast<void**>(&d_tab), 8 * (5ull * count + 1), st), "alloc")) {
       ret = LORENZ_E_CUDA; break;
     }
     if (!cuda_ok(cudaMemcpyAsync(d_keys, h_keys.data(), sizeof(lz::DevKey) * count, cudaMemcpyHostToDevice, st),
@@ -882,7 +927,6 @@ lorenz_status lorenz_power_spectrum(const uint8_t* x, uint32_t H, uint32_t W, do
   lorenz_status ret = spectra_args(x, H, W, power);
   if (ret != LORENZ_OK) return ret;
   cudaStream_t st = (cudaStream_t)stream;
-  keep_pool_cached();
   const uint64_t N = (uint64_t)H * W;
   double2* ws = nullptr;
   double2* part = nullptr;
@@ -893,7 +937,7 @@ lorenz_status lorenz_power_spectrum(const uint8_t* x, uint32_t H, uint32_t W, do
   const bool r2c = W >= 4;
   const uint32_t M = r2c ? W / 2 : W;
   const uint64_t NW = (uint64_t)H * M;
-  if (!cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&ws), NW * sizeof(double2), st), "alloc fft"))
+  if (!cuda_ok(lz::lib_malloc_async(reinterpret_cast<void**>(&ws), NW * sizeof(double2), st), "alloc fft"))
     return LORENZ_E_CUDA;
   lz::FftPass rows = fft_rows(H, M, W, M), cols = fft_cols(H, M, M, W);
   rows.W = cols.W = W;
@@ -901,7 +945,7 @@ lorenz_status lorenz_power_spectrum(const uint8_t* x, uint32_t H, uint32_t W, do
   const uint32_t tiles = (cols.nseq + cols.S - 1) / cols.S;  // >= the column pass's grid
   unsigned nparts = 0;                                          // one flatness partial per column CTA
   bool ok = !flatness ||
-            cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&part), tiles * sizeof(double2), st), "alloc");
+            cuda_ok(lz::lib_malloc_async(reinterpret_cast<void**>(&part), tiles * sizeof(double2), st), "alloc");
   cols.part = flatness ? part : nullptr;
   if (r2c)
     ok = ok &&
@@ -927,7 +971,6 @@ lorenz_status lorenz_autocorrelation(const uint8_t* x, uint32_t H, uint32_t W, d
   lorenz_status ret = spectra_args(x, H, W, r);
   if (ret != LORENZ_OK) return ret;
   cudaStream_t st = (cudaStream_t)stream;
-  keep_pool_cached();
   const uint64_t N = (uint64_t)H * W;
   double2* ws = nullptr;
   unsigned long long* aux = nullptr;  // [0] = byte sum, [1] = lag-0 value (double bits)
@@ -938,8 +981,8 @@ lorenz_status lorenz_autocorrelation(const uint8_t* x, uint32_t H, uint32_t W, d
   const bool r2c = W >= 4;
   const uint32_t M = r2c ? W / 2 : W;
   const uint64_t Pw = r2c ? M : fft_ws_pitch(W), NW = (uint64_t)H * Pw;
-  if (!cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&ws), NW * sizeof(double2), st), "alloc fft") ||
-      !cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&aux), 16, st), "alloc aux")) {
+  if (!cuda_ok(lz::lib_malloc_async(reinterpret_cast<void**>(&ws), NW * sizeof(double2), st), "alloc fft") ||
+      !cuda_ok(lz::lib_malloc_async(reinterpret_cast<void**>(&aux), 16, st), "alloc aux")) {
     if (ws) cudaFreeAsync(ws, st);
     return LORENZ_E_CUDA;
   }
@@ -982,14 +1025,13 @@ namespace {
 template <typename Launch>
 lorenz_status span_launch(const lorenz_span* spans, uint32_t count, uint64_t* out, uint64_t out_words,
                           cudaStream_t st, Launch launch) {
-  keep_pool_cached();
   if (!cuda_ok(cudaMemsetAsync(out, 0, sizeof(uint64_t) * out_words, st), "memset")) return LORENZ_E_CUDA;
   uint64_t mx = 0;
   for (uint32_t i = 0; i < count; ++i) mx = spans[i].len > mx ? spans[i].len : mx;
   const uint64_t tiles = (mx + lz::kStatTile - 1) / lz::kStatTile;
   if (!tiles) return LORENZ_OK;
   lorenz_span* d = nullptr;
-  if (!cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&d), sizeof(lorenz_span) * count, st), "alloc spans"))
+  if (!cuda_ok(lz::lib_malloc_async(reinterpret_cast<void**>(&d), sizeof(lorenz_span) * count, st), "alloc spans"))
     return LORENZ_E_CUDA;
   lorenz_status ret = LORENZ_OK;
   if (!cuda_ok(cudaMemcpyAsync(d, spans, sizeof(lorenz_span) * count, cudaMemcpyHostToDevice, st), "spans H2D"))
@@ -1037,7 +1079,6 @@ struct HostPipe {
   // The streams and events are created once per host thread and device (host_pipe below):
   // creating eight streams per call cost ~0.6 ms, 2 % of a 64 MiB call.
   bool init() {
-    keep_pool_cached();  // freed stream-ordered memory stays cached across calls
     for (int i = 0; i < kStreams; ++i) {
       if (!cuda_ok(cudaStreamCreateWithFlags(&st[i], cudaStreamNonBlocking), "stream create")) return false;
       if (!cuda_ok(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming), "event create")) return false;
@@ -1193,9 +1234,9 @@ static lorenz_status host_range(const lorenz_key* k, uint64_t n, uint64_t B0, ui
   lorenz_result* d_res = nullptr;
   cudaStream_t s0 = P.st[0];
   for (uint32_t i = 0; i < S && ret == LORENZ_OK; ++i)
-    if (!cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&d_in[i]), cap_in, s0), "alloc in") ||
-        !cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&d_out[i]), cap_out, s0), "alloc out") ||
-        (decrypt && !cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&d_ok[i]), cap_blk, s0), "alloc ok")))
+    if (!cuda_ok(lz::lib_malloc_async(reinterpret_cast<void**>(&d_in[i]), cap_in, s0), "alloc in") ||
+        !cuda_ok(lz::lib_malloc_async(reinterpret_cast<void**>(&d_out[i]), cap_out, s0), "alloc out") ||
+        (decrypt && !cuda_ok(lz::lib_malloc_async(reinterpret_cast<void**>(&d_ok[i]), cap_blk, s0), "alloc ok")))
       ret = LORENZ_E_CUDA;
   if (ret == LORENZ_OK) ret = alloc_result(&d_res, s0);
   if (ret == LORENZ_OK) {

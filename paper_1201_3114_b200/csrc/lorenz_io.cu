@@ -15,6 +15,7 @@
 #include <condition_variable>
 #include <cstdio>
 #include <cstdlib>
+#include <algorithm>
 #include <cstring>
 #include <deque>
 #include <mutex>
@@ -186,7 +187,7 @@ lorenz_status stream_pass(const lorenz_key* k, uint64_t n, bool decrypt, FILE* i
   if (cb == 0) cb = 1;
   if (cb > nb) cb = nb;
   const uint64_t pt_cap = fast ? cb * B : n, ct_cap = pt_cap + 16 * cb;
-  const bool trace = std::getenv("LORENZ_IO_TRACE") != nullptr;
+  static const bool trace = std::getenv("LORENZ_IO_TRACE") != nullptr;  // debug timeline, read once
   const double t_start = now_s();
   Pipe P;
   lorenz_status r = decrypt ? P.init(ct_cap, pt_cap, out) : P.init(pt_cap, ct_cap, out);
@@ -266,11 +267,14 @@ lorenz_status lorenz_envelope_read(const uint8_t* hdr, size_t len, lorenz_params
   p->block_size = chunk;
   p->integrator = integ;
   p->variant = variant;
-  *n = get_le(hdr + 16, 8);
-  if (ct_len) {
-    const uint64_t nb = mode == LORENZ_STRONG ? 1 : ((*n + chunk - 1) / chunk ? (*n + chunk - 1) / chunk : 1);
-    *ct_len = *n + 16 * nb;
-  }
+  const uint64_t pn = get_le(hdr + 16, 8);
+  // block count and body length of an untrusted payload length, without wrapping: a header
+  // whose file would exceed 2^64 bytes is malformed
+  const uint64_t nb = mode == LORENZ_STRONG ? 1 : std::max<uint64_t>(1, pn / chunk + (pn % chunk != 0));
+  if (nb > (UINT64_MAX - LORENZ_ENVELOPE_BYTES) / 16 || pn > UINT64_MAX - LORENZ_ENVELOPE_BYTES - 16 * nb)
+    return LORENZ_E_FORMAT;
+  *n = pn;
+  if (ct_len) *ct_len = pn + 16 * nb;
   return LORENZ_OK;
 }
 

@@ -20,7 +20,7 @@ cudaError_t launch_seg(const DevConst& C, const SegPlan& P, const DevKey& K, con
   const size_t hdr = (4 * ((size_t)P.slots + 2) + 15) & ~(size_t)15;  // ticket + S + 1 flags
   const size_t bytes = hdr + ((size_t)P.slots + 1) * kSegWords * 32 * 8;
   uint8_t* scr = nullptr;
-  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&scr), bytes, st);
+  cudaError_t e = lib_malloc_async(reinterpret_cast<void**>(&scr), bytes, st);
   if (e == cudaErrorMemoryAllocation) {  // no room for the hand-over scratch: take the wave kernel
     (void)cudaGetLastError();
     return cudaErrorNotReady;

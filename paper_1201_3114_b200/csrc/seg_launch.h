@@ -7,6 +7,10 @@
 #include "lorenz_device.cuh"
 
 namespace lz {
+// Stream-ordered allocation from the library's own per-device pool (lorenz.cu); free with
+// cudaFreeAsync.
+cudaError_t lib_malloc_async(void** p, size_t bytes, cudaStream_t st);
+
 // Enqueue one balanced launch on `st`: a pool allocation for the hand-over scratch, a memset of
 // its ticket and flags, the kernel (one CTA of `cta` threads per SM), the free. Returns
 // cudaErrorNotReady (nothing enqueued) when the scratch cannot be allocated: take the wave kernel.

@@ -95,6 +95,11 @@ class CudaEngine:
         self.L.lorenz_decrypt_async(self.key, self.n, b0, b1, ct, pt, self.res, stream=stream)
         return self.first_bad()
 
+    def verify(self, b0, b1, ct, stream=None) -> torch.Tensor:
+        self.L.lorenz_result_init_async(self.res, stream)
+        self.L.lorenz_verify_async(self.key, self.n, b0, b1, ct, self.res, stream)
+        return self.first_bad()
+
     def first_bad(self) -> torch.Tensor:
         fb = self.res[16:24].view(torch.int64).clone()  # UINT64_MAX reads as -1
         return torch.where(fb < 0, torch.full_like(fb, NO_BAD), fb)

@@ -31,7 +31,7 @@ EXPORTS = ["lorenz_abi_version", "lorenz_last_error", "lorenz_status_string", "l
            "lorenz_compare_spans", "lorenz_histograms", "lorenz_envelope_write", "lorenz_envelope_read",
            "lorenz_encrypt_file", "lorenz_decrypt_file", "lorenz_digit_histograms",
            "lorenz_autocorrelation", "lorenz_power_spectrum", "lorenz_encrypt_ragged", "lorenz_decrypt_ragged",
-           "lorenz_launch_plan"]
+           "lorenz_launch_plan", "lorenz_set_tuning"]
 E_IO, E_FORMAT = 7, 8
 ENVELOPE_BYTES = 24
 
@@ -91,6 +91,7 @@ def lib():
         L.lorenz_ct_len.restype = u64
         L.lorenz_pt_len.argtypes = [kp, u64, C.POINTER(u64)]
         L.lorenz_launch_plan.argtypes = [kp, u64, u64, u64, C.POINTER(lorenz_plan)]
+        L.lorenz_set_tuning.argtypes = [C.POINTER(lorenz_tuning)]
         L.lorenz_encrypt.argtypes = [kp, u64, u64, u64, vp, vp, vp, vp]
         L.lorenz_decrypt.argtypes = [kp, u64, u64, u64, vp, vp, C.POINTER(C.c_int64), vp, vp]
         L.lorenz_verify.argtypes = [kp, u64, u64, u64, vp, C.POINTER(C.c_int64), vp, vp]
@@ -189,6 +190,36 @@ def lorenz_launch_plan(key: Key, n: int, b0: int, b1: int) -> dict:
     _check(lib().lorenz_launch_plan(C.byref(key.raw), n, b0, b1, C.byref(p)), "lorenz_launch_plan")
     return {"kind": ("wave", "balanced")[p.kind], "cta": p.cta, "grid": p.grid, "lanes": p.lanes,
             "slots": p.slots, "chunks_per_slot": p.chunks_per_slot, "chunks_skew": p.chunks_skew}
+
+
+class lorenz_tuning(C.Structure):
+    _fields_ = [("schedule", C.c_uint32), ("seg_slots", C.c_uint32), ("seg_skew", C.c_int32), ("cta", C.c_uint32)]
+
+
+SCHED_AUTO, SCHED_WAVE, SCHED_BALANCED = 0, 1, 2
+
+
+def lorenz_set_tuning(schedule: int = SCHED_AUTO, seg_slots: int = 0, seg_skew: int = -1, cta: int = 0,
+                      reset: bool = False):
+    """Process-wide launch-plan overrides for tests and tuning (lorenz.h); reset=True restores
+    the defaults."""
+    t = None if reset else C.byref(lorenz_tuning(schedule, seg_slots, seg_skew, cta))
+    _check(lib().lorenz_set_tuning(t), "lorenz_set_tuning")
+
+
+class tuning:
+    """Context manager over lorenz_set_tuning: `with L.tuning(schedule=L.SCHED_BALANCED, seg_slots=3): ...`
+    restores the defaults on exit."""
+
+    def __init__(self, **kw):
+        self.kw = kw
+
+    def __enter__(self):
+        lorenz_set_tuning(**self.kw)
+        return self
+
+    def __exit__(self, *exc):
+        lorenz_set_tuning(reset=True)
 
 
 def lorenz_num_blocks(key: Key, n: int) -> int:

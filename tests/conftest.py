@@ -21,3 +21,22 @@ def ref():
     import oracle
     oracle.lib()
     return oracle
+
+
+@pytest.fixture
+def tune():
+    """Launch-plan overrides through the C ABI (lorenz_set_tuning): tune(schedule="wave"|"seg"|None,
+    seg_slots=S|None, seg_skew=k|None, cta=C|None); None restores that field's default. Every
+    override is cleared when the test ends."""
+    from paper_1201_3114_b200 import lorenz as L
+    state = {}
+    codes = {None: L.SCHED_AUTO, "wave": L.SCHED_WAVE, "seg": L.SCHED_BALANCED}
+    defaults = {"schedule": None, "seg_slots": 0, "seg_skew": -1, "cta": 0}
+
+    def set_(**kw):
+        state.update(kw)
+        args = {k: (defaults[k] if state.get(k) is None and k != "schedule" else state.get(k)) for k in defaults}
+        args["schedule"] = codes[args["schedule"]]
+        L.lorenz_set_tuning(**args)
+    yield set_
+    L.lorenz_set_tuning(reset=True)

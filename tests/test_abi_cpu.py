@@ -105,12 +105,11 @@ def test_product_never_imports_oracle():
                 assert "lorenz_ref" not in txt, f
 
 
-def test_launch_plan_rules(L, monkeypatch):
+def test_launch_plan_rules(L, tune):
     """Host-side schedule choice, computed without a device (148 SMs): the
     balanced kernel for 2+ warps per SM sub-partition and under three waves unless the wave
     kernel's single wave splits evenly; the wave kernel otherwise; overrides honoured."""
-    monkeypatch.delenv("LORENZ_SCHED", raising=False)
-    monkeypatch.delenv("LORENZ_SEG_SLOTS", raising=False)
+    tune()
     key = L.lorenz_keysetup(b"0123456789abcdef", mode=L.FAST)
     plan = lambda blocks: L.lorenz_launch_plan(key, blocks * 1024, 0, blocks)
     p = plan(65536)  # C3: 2,048 units, 3.46 warps per sub-partition in one wave
@@ -128,23 +127,21 @@ def test_launch_plan_rules(L, monkeypatch):
     assert L.lorenz_launch_plan(key, 0, 0, 1)["lanes"] == 1
     fma = L.lorenz_keysetup(b"0123456789abcdef", mode=L.FAST, integrator=L.RK4_FMA)
     assert L.lorenz_launch_plan(fma, 65536 * 1024, 0, 65536)["kind"] == "balanced"
-    monkeypatch.setenv("LORENZ_SCHED", "wave")
+    tune(schedule="wave")
     assert plan(65536)["kind"] == "wave"
-    monkeypatch.setenv("LORENZ_SCHED", "seg")
-    monkeypatch.setenv("LORENZ_SEG_SLOTS", "3")
+    tune(schedule="seg", seg_slots=3)
     p = plan(160)
     assert p["kind"] == "balanced" and p["slots"] == 3 and p["chunks_per_slot"] == 109 and p["chunks_skew"] == 0
     with pytest.raises(L.LorenzError):
         L.lorenz_launch_plan(key, 1024, 0, 2)
 
 
-def test_launch_plan_mcnaughton_invariants(L, monkeypatch):
+def test_launch_plan_mcnaughton_invariants(L, tune):
     """For every balanced plan: slots <= units (else a slot would hold less than one unit),
     every slot holds >= Q = (B+16)/16 chunks (a cut unit's two pieces then never overlap in time;
     skewed plans keep Q/8 more), the slots cover the U * Q chunk line without a spare slot's worth,
     and the grid holds every slot."""
-    monkeypatch.delenv("LORENZ_SCHED", raising=False)
-    monkeypatch.delenv("LORENZ_SEG_SLOTS", raising=False)
+    tune()
     import random
     rng = random.Random(5)
     for B in (1024, 2048, 65536):
@@ -170,3 +167,50 @@ def test_launch_plan_mcnaughton_invariants(L, monkeypatch):
                 assert p["chunks_per_slot"] >= q + q // 8  # slack: the pieces of a cut unit never meet
             assert min(caps) >= q
             assert sum(caps) >= units * q > sum(caps) - len(caps) - p["grid"] * wpc * p["chunks_skew"]
+
+
+def test_set_tuning_validated(L):
+    """lorenz_set_tuning (the library reads no environment variables): out-of-range fields are
+    rejected and change nothing; NULL restores the defaults."""
+    key = L.lorenz_keysetup(b"0123456789abcdef", mode=L.FAST)
+    default = L.lorenz_launch_plan(key, 65536 * 1024, 0, 65536)
+    for bad in (dict(schedule=3), dict(cta=100), dict(seg_skew=-2), dict(seg_skew=101)):
+        with pytest.raises(L.LorenzError) as e:
+            L.lorenz_set_tuning(**bad)
+        assert e.value.status == L.E_ARG
+    assert L.lorenz_launch_plan(key, 65536 * 1024, 0, 65536) == default
+    with L.tuning(schedule=L.SCHED_WAVE, cta=512):
+        p = L.lorenz_launch_plan(key, 65536 * 1024, 0, 65536)
+        assert p["kind"] == "wave" and p["cta"] == 512
+    assert L.lorenz_launch_plan(key, 65536 * 1024, 0, 65536) == default
+
+
+def test_async_result_and_batch_tags_alignment(L):
+    """The kernels update `res` and the batch tags with 64-bit atomics: a pointer that is not
+    16-byte aligned is an argument error, reported before anything is enqueued (no device here)."""
+    key = L.lorenz_keysetup(b"0123456789abcdef", mode=L.FAST)
+    lib, kp = L.lib(), C.byref(key.raw)
+    pt, ct = 0x7F0000000000, 0x7F0010000000
+    for res in (0x7F0020000008, 0x7F0020000001):
+        assert lib.lorenz_encrypt_async(kp, 4096, 0, 4, pt, ct, res, None) == L.E_ARG
+        assert lib.lorenz_decrypt_async(kp, 4096, 0, 4, ct, pt, None, res, None) == L.E_ARG
+        assert lib.lorenz_verify_async(kp, 4096, 0, 4, ct, res, None) == L.E_ARG
+        assert lib.lorenz_result_init_async(res, None) == L.E_ARG
+    keys = (L.lorenz_key * 2)(key.raw, key.raw)
+    assert lib.lorenz_encrypt_batch(keys, 2, 4096, pt, ct, 0x7F0020000008, None) == L.E_ARG
+
+
+def test_ragged_overlap_not_hidden_by_an_empty_message(L):
+    """Decrypt outputs A = [0, 4096), B = [16, 16) (a zero-length message), C = [1024, 2048):
+    A and C overlap; the empty range sorted between them must not hide it."""
+    import numpy as np
+    key = L.lorenz_keysetup(b"0123456789abcdef", mode=L.FAST)
+    keys = (L.lorenz_key * 3)(key.raw, key.raw, key.raw)
+    n = np.array([4096, 0, 1024], dtype=np.uint64)
+    ct_off = np.array([0, 8192, 12288], dtype=np.uint64)
+    pt_off = np.array([0, 16, 1024], dtype=np.uint64)
+    fb = np.zeros(3, dtype=np.int64)
+    st = L.lib().lorenz_decrypt_ragged(keys, 3, n.ctypes.data, ct_off.ctypes.data, pt_off.ctypes.data,
+                                       0x7F0000000000, 0x7F0010000000, 0x7F0020000000, fb.ctypes.data, None)
+    assert st == L.E_ARG
+    assert b"overlap" in L.lib().lorenz_last_error()

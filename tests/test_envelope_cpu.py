@@ -57,3 +57,26 @@ def test_header_errors(L):
         with pytest.raises(L.LorenzError) as e:
             L.lorenz_envelope_read(hdr)
         assert e.value.status == st
+
+
+def test_untrusted_payload_length_does_not_wrap(L):
+    """A header whose payload length would make the file exceed 2^64 bytes is malformed
+    (E_FORMAT), not a wrapped ciphertext length."""
+    import struct
+    key = L.lorenz_keysetup(b"envelope-pw", mode=L.FAST)
+    hdr = bytearray(L.lorenz_envelope_write(key, 5))
+    for bad in (2 ** 64 - 16, 2 ** 64 - 1, 2 ** 64 - 24 - 16 * (2 ** 64 // 1040)):
+        hdr[16:24] = struct.pack("<Q", bad)
+        with pytest.raises(L.LorenzError) as e:
+            L.lorenz_envelope_read(bytes(hdr))
+        assert e.value.status == L.E_FORMAT
+    # the largest representable payload is still accepted
+    big = (2 ** 64 - 1 - 24) // 1040 * 1024
+    hdr[16:24] = struct.pack("<Q", big)
+    p, n, ctl = L.lorenz_envelope_read(bytes(hdr))
+    assert n == big and ctl == big + 16 * (big // 1024)
+    sk = L.lorenz_keysetup(b"envelope-pw", mode=L.STRONG)
+    hdr = bytearray(L.lorenz_envelope_write(sk, 5))
+    hdr[16:24] = struct.pack("<Q", 2 ** 64 - 40)
+    with pytest.raises(L.LorenzError):
+        L.lorenz_envelope_read(bytes(hdr))

@@ -15,6 +15,7 @@ five configs"). Byte-for-byte, tolerance 0:
 The oracle runs on every host core (oracle/lorenz_ref.c, static block partition); C4 costs
 about 3.5 minutes of the 16-core box's time.
 """
+import json
 import os
 import random
 from concurrent.futures import ThreadPoolExecutor
@@ -102,7 +103,8 @@ def test_c4_full_message_and_rank_slices():
     n = 1 << 30
     key, pw, msg, want, want_tag = full_message_parity(n, 100)
     nb = key.num_blocks(n)
-    assert want_tag.hex() == "d869add9eeb966135b7b30a7dd977de0"  # the bench's validated.tag_xor
+    golden = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "oracle_tags.json")))
+    assert want_tag.hex() == golden["c4/n_it=100/rk4"]  # what bench.py checks at every rank count
     pt = torch.from_numpy(msg).to(DEV)
     wv = want.reshape(nb, B + 16)
     # the driver's scaling runs: each rank launches its own slice (its own balanced plan)

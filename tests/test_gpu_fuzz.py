@@ -60,11 +60,11 @@ def test_random_configurations(seed):
 
 
 @pytest.mark.parametrize("seed", range(3))
-def test_random_configurations_balanced_kernel(seed, monkeypatch):
+def test_random_configurations_balanced_kernel(seed, tune):
     """The same parity through the balanced kernel, forced onto a random number of warp slots
     (so units are cut at random chunk positions): FAST messages of 33-420 blocks, random block
     sizes, block ranges, integrators, step sizes and Step-3 variants."""
-    monkeypatch.setenv("LORENZ_SCHED", "seg")
+    tune(schedule="seg")
     rng = random.Random(7000 + seed)
     for _ in range(25):
         B = rng.choice([1024, 1040, 1024 + 16 * rng.randrange(1, 64)])
@@ -80,7 +80,7 @@ def test_random_configurations_balanced_kernel(seed, monkeypatch):
         b0 = rng.choice([0, rng.randrange(nb // 2)])
         b1 = nb if rng.random() < 0.5 else rng.randrange(b0 + 1, nb + 1)
         units = -(-(b1 - b0) // 32)
-        monkeypatch.setenv("LORENZ_SEG_SLOTS", str(rng.randrange(1, units + 1)))
+        tune(seg_slots=rng.randrange(1, units + 1))
         p = key.params
         prm = oracle.params(mode=p.mode, n_it=p.n_it, dt_code=p.dt_code, block_size=p.block_size,
                             integrator=p.integrator, variant=p.variant)

@@ -35,8 +35,19 @@ def test_two_ranks_one_gpu_gloo(workload):
     d2 = json.loads(two[0])
     assert d2["n_gpus"] == 2 and d2["value"] > 0 and d2["clocks"]["sm_mhz"] > 0
     if workload in ("c3", "c4"):  # c4: the driver's N = 2 slices (512 MiB each, balanced kernel)
-        assert d2["validated"]["round_trip"] is True
-        assert d2["e2e"]["matches_device_ct"] is True
+        v = d2["validated"]
+        assert v["round_trip"] is True and v["verify_ok"] is True
+        assert d2["e2e"]["matches_device_ct"] is True and d2["decrypt_e2e"]["round_trip"] is True
+        # the fields the driver's scaling runs are checked by: the communicator's rank count,
+        # every rank's slice, kernel time and digest, and the combined digest = the oracle's
+        rk = d2["ranks"]
+        assert rk["world_size"] == 2 and len(rk["per_rank"]) == 2
+        assert [r["rank"] for r in rk["per_rank"]] == [0, 1]
+        assert rk["per_rank"][0]["blocks"][1] == rk["per_rank"][1]["blocks"][0]
+        assert rk["kernel_ms_max"] >= rk["kernel_ms_min"] > 0
+        comb = bytes(a ^ b for a, b in zip(*(bytes.fromhex(r["tag"]) for r in rk["per_rank"])))
+        assert comb.hex() == v["tag_xor"]
+        assert v["oracle_tag_xor"] and v["tag_matches_oracle"] is True
         one = run([sys.executable] + args + ["--gpus", "1"], os.environ.copy())
         d1 = json.loads(one[-1])
         assert d1["validated"]["tag_xor"] == d2["validated"]["tag_xor"]

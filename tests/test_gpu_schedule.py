@@ -3,7 +3,7 @@
 `lorenz_chain_seg_kernel` cuts the launch's 32-chain units at slot boundaries and hands the
 32 chain states of a cut unit from one warp to another through global memory.
 The library picks it for launches with >= 2 warps of chains per SM sub-partition; here
-LORENZ_SEG_SLOTS forces small slot counts so that small messages — ones the oracle checks
+lorenz_set_tuning forces small slot counts so that small messages — ones the oracle checks
 byte for byte — are cut at many places: unit boundaries, mid-window, the sentinel, a ragged
 last block. Integer outputs, tolerance 0, against the oracle and against the wave kernel.
 """
@@ -20,19 +20,11 @@ DEV = torch.device("cuda:0")
 
 
 @pytest.fixture
-def sched(monkeypatch):
-    """Set the schedule overrides for this test (the library reads them at every launch)."""
+def sched(tune):
+    """Set the schedule overrides for this test (lorenz_set_tuning; cleared afterwards)."""
     def set_(slots=None, mode=None):
-        if slots is None:
-            monkeypatch.delenv("LORENZ_SEG_SLOTS", raising=False)
-        else:
-            monkeypatch.setenv("LORENZ_SEG_SLOTS", str(slots))
-        if mode is None:
-            monkeypatch.delenv("LORENZ_SCHED", raising=False)
-        else:
-            monkeypatch.setenv("LORENZ_SCHED", mode)
-    yield set_
-    set_()
+        tune(seg_slots=slots, schedule=mode)
+    return set_
 
 
 def oparams(key):
@@ -308,7 +300,7 @@ def test_seg_concurrent_launches_with_a_full_gpu_kernel(sched):
 
 
 @pytest.mark.parametrize("blocks,skew", [(40000, 8), (56000, 30), (65536, 60), (100000, 15), (140000, 120)])
-def test_seg_skewed_slots_equal_wave(sched, monkeypatch, blocks, skew):
+def test_seg_skewed_slots_equal_wave(sched, tune, blocks, skew):
     """Skewed slot capacities (later warp groups of a CTA get more chunks) at default slot
     layouts, including skews far above the tuned 8 per mille: ciphertext, tag and verdicts equal
     the wave kernel's, and sampled blocks equal the oracle's."""
@@ -318,7 +310,7 @@ def test_seg_skewed_slots_equal_wave(sched, monkeypatch, blocks, skew):
     key = L.lorenz_keysetup(pw, mode=L.FAST, n_it=3)
     nb = key.num_blocks(n)
     pt = torch.from_numpy(msg).to(DEV)
-    monkeypatch.setenv("LORENZ_SEG_SKEW", str(skew))
+    tune(seg_skew=skew)
     sched(mode="seg")
     p = L.lorenz_launch_plan(key, n, 0, nb)
     assert p["kind"] == "balanced"
