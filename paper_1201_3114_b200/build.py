@@ -31,11 +31,26 @@ def nvcc() -> str:
     return "nvcc"
 
 
+STAMP = LIB + ".srchash"  # hash of the sources the library was built from (travels with it)
+
+
+def source_hash() -> str:
+    """SHA-256 over the library's sources, headers and flags. Content-based, so a copy of the
+    tree (a GPU box's snapshot, where file times are the copy's) does not look stale."""
+    import hashlib
+    h = hashlib.sha256(" ".join(NVCC_FLAGS).encode())
+    for f in sorted(SOURCES + HEADERS + ["lorenz_cli.cpp"]):
+        h.update(f.encode())
+        with open(os.path.join(CSRC, f), "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()
+
+
 def stale() -> bool:
-    if not os.path.exists(LIB):
+    if not (os.path.exists(LIB) and os.path.exists(STAMP) and os.path.exists(CLI)):
         return True
-    t = os.path.getmtime(LIB)
-    return any(os.path.getmtime(os.path.join(CSRC, f)) > t for f in SOURCES + HEADERS)
+    with open(STAMP) as fh:
+        return fh.read().strip() != source_hash()
 
 
 def compile_lib(out: str, defines=()) -> str:
@@ -72,6 +87,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     with open(os.path.join(CSRC, "ptxas.log"), "w") as f:
         f.write(log)
     build_cli()
+    with open(STAMP, "w") as f:
+        f.write(source_hash() + "\n")
     return LIB
 
 
