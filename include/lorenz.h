@@ -24,7 +24,9 @@
  *     the operation order of DESIGN.md §2, so results are bit-identical on every
  *     conforming implementation (and to the CPU oracle in oracle/).
  *   - Device pointers are plain CUDA device addresses (e.g. torch.Tensor.data_ptr()),
- *     16-byte aligned; the caller owns every buffer. `cuda_stream` is a cudaStream_t
+ *     16-byte aligned; the caller owns every buffer. Any device-accessible address works,
+ *     including mapped page-locked host memory (UVA): the chain kernels then read and write
+ *     it over PCIe themselves, window by window (the direct mode of lorenz_encrypt_host). `cuda_stream` is a cudaStream_t
  *     (NULL = legacy default stream). Calls without the _async suffix enqueue their
  *     work on that stream and synchronise it before returning.
  *   - Errors are returned, never raised: no abort/exit. Argument errors are reported
@@ -140,7 +142,7 @@ const char* lorenz_status_string(lorenz_status s);
  *              balanced kernel (any size, RK4 / Euler / RK4-FMA);
  *   seg_slots  balanced kernel: warp slots (0 = SMs x warps per CTA; clamped to the 32-block
  *              units, so every unit spans at most two slots);
- *   seg_skew   balanced kernel: slot skew per warp group in per mille of a slot (-1 = the
+ *   seg_skew   balanced kernel: slot skew per warp group in per mille of a slot, 0..1000 (-1 = the
  *              default 8, 0 = equal slots);
  *   cta        wave kernel: threads per CTA (0 = automatic; 128, 256 or 512).
  * t = NULL restores every default. Thread-safe; applies to plans made after the call.

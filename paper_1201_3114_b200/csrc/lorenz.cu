@@ -436,7 +436,7 @@ lorenz_status lorenz_keysetup(const uint8_t* pw, size_t pw_len, const lorenz_par
 lorenz_status lorenz_set_tuning(const lorenz_tuning* t) {
   lorenz_tuning v = {0, 0, -1, 0};
   if (t) {
-    if (t->schedule > 2 || t->seg_skew < -1 || t->seg_skew > 100 ||
+    if (t->schedule > 2 || t->seg_skew < -1 || t->seg_skew > 1000 ||
         (t->cta && t->cta != 128 && t->cta != 256 && t->cta != 512))
       return LORENZ_E_ARG;
     v = *t;

@@ -91,8 +91,10 @@ class Batch:
         self.hist = torch.empty(256 * T, dtype=torch.int64, device=dev)
         self.lsb = torch.empty(3 * len(self.lsb_spans), dtype=torch.int64, device=dev)
 
-    def encrypt(self, stream=None):
-        L.lorenz_encrypt_batch(self.keys, self.n, self.pts, self.cts, self.tags, stream)
+    def encrypt(self, stream=None, pts=None):
+        """One batched launch. pts: the plaintexts (default: the device copy); a pinned host tensor
+        is read by the kernel over PCIe (mapped pinned memory is device-accessible)."""
+        L.lorenz_encrypt_batch(self.keys, self.n, self.pts if pts is None else pts, self.cts, self.tags, stream)
 
     def statistics(self, stream=None):
         L.lorenz_compare_spans(self.cts, self.cts, self.spans, self.cmp_out, stream)

@@ -174,7 +174,7 @@ def test_set_tuning_validated(L):
     rejected and change nothing; NULL restores the defaults."""
     key = L.lorenz_keysetup(b"0123456789abcdef", mode=L.FAST)
     default = L.lorenz_launch_plan(key, 65536 * 1024, 0, 65536)
-    for bad in (dict(schedule=3), dict(cta=100), dict(seg_skew=-2), dict(seg_skew=101)):
+    for bad in (dict(schedule=3), dict(cta=100), dict(seg_skew=-2), dict(seg_skew=1001)):
         with pytest.raises(L.LorenzError) as e:
             L.lorenz_set_tuning(**bad)
         assert e.value.status == L.E_ARG
