@@ -96,12 +96,15 @@ class Batch:
         is read by the kernel over PCIe (mapped pinned memory is device-accessible)."""
         L.lorenz_encrypt_batch(self.keys, self.n, self.pts if pts is None else pts, self.cts, self.tags, stream)
 
-    def statistics(self, stream=None):
+    def statistics(self, stream=None, pts=None):
+        """pts: the plaintexts the LSB statistic reads (default: the device copy; a pinned host
+        tensor is read over PCIe)."""
+        src = self.pts if pts is None else pts
         L.lorenz_compare_spans(self.cts, self.cts, self.spans, self.cmp_out, stream)
         L.lorenz_histograms(self.cts, self.hist_spans, self.hist, stream)
         for c0 in range(0, len(self.lsb_spans), 65535):
             part = self.lsb_spans[c0:c0 + 65535]
-            L.lorenz_compare_spans(self.cts, self.pts, part, self.lsb[3 * c0:3 * (c0 + len(part))], stream)
+            L.lorenz_compare_spans(self.cts, src, part, self.lsb[3 * c0:3 * (c0 + len(part))], stream)
 
     def results(self):
         T, nb, B = self.T, self.nb, self.B

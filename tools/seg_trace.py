@@ -29,11 +29,13 @@ def main():
     ap.add_argument("--kib", type=int, nargs="+", default=[65536, 100000, 131072])
     ap.add_argument("--n-it", type=int, default=100)
     ap.add_argument("--dump", default=None, help="write the raw per-slot rows (npz) here")
+    ap.add_argument("--integrator", choices=["rk4", "euler", "rk4fma"], default="rk4")
     a = ap.parse_args()
     dev = torch.device("cuda:0")
     lib = L.lib()
     lib.lorenz_debug_seg_trace.argtypes = [C.c_void_p]
-    key = L.lorenz_keysetup(inputs.password(), mode=L.FAST, n_it=a.n_it)
+    key = L.lorenz_keysetup(inputs.password(), mode=L.FAST, n_it=a.n_it,
+                            integrator={"rk4": L.RK4, "euler": L.EULER, "rk4fma": L.RK4_FMA}[a.integrator])
     big = max(a.kib) << 10
     msg = torch.from_numpy(inputs.message(big)).to(dev)
     ct = torch.empty(key.ct_len(big), dtype=torch.uint8, device=dev)
@@ -73,6 +75,9 @@ def main():
             "first_piece_done_ms_p50_p100": [round(float(np.percentile(first[first > -t0], q)) / 1e6, 3)
                                              for q in (50, 100)] if (rows[:, 1] > 0).any() else None,
             "warpid_mod4_counts": np.bincount((wid % 4).astype(np.int64), minlength=4).tolist(),
+            # mean finish time per warp index within the CTA (t = start order): rate differences
+            "finish_ms_by_warp_in_cta": [round(float(fin[(rows[:, 7] % (int(used.sum()) // 148)) == w].mean()) / 1e6, 3)
+                                         for w in range(int(used.sum()) // 148)],
             "sms": int(len(np.unique(sm))),
         }), flush=True)
     if a.dump:

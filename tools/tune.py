@@ -27,7 +27,12 @@ def main():
     ap.add_argument("--n-it", type=int, default=100)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--integrator", choices=["rk4", "euler", "rk4fma"], default="rk4")
+    ap.add_argument("--sched", choices=["auto", "wave", "seg"], default="auto")
+    ap.add_argument("--slots", type=int, default=0, help="balanced-kernel warp slots (0 = default)")
+    ap.add_argument("--skew", type=int, default=-1, help="balanced-kernel skew per mille (-1 = default)")
     a = ap.parse_args()
+    L.lorenz_set_tuning(schedule={"auto": L.SCHED_AUTO, "wave": L.SCHED_WAVE, "seg": L.SCHED_BALANCED}[a.sched],
+                        seg_slots=a.slots, seg_skew=a.skew)
     dev = torch.device("cuda:0")
     integ = {"rk4": L.RK4, "euler": L.EULER, "rk4fma": L.RK4_FMA}[a.integrator]
     key = L.lorenz_keysetup(inputs.password(), mode=L.FAST, n_it=a.n_it, integrator=integ)
@@ -52,7 +57,7 @@ def main():
             ts.append(e0.elapsed_time(e1) / 1e3)
         t = min(ts)
         ops = fp64_ops(n, 1024, 0, nb, a.n_it, a.integrator)
-        print(json.dumps({"tag": a.tag, "integrator": a.integrator, "mib": round(n / 2**20, 3), "blocks": nb, "ms": round(t * 1e3, 3),
+        print(json.dumps({"tag": a.tag, "integrator": a.integrator, "plan": L.lorenz_launch_plan(key, n, 0, nb), "mib": round(n / 2**20, 3), "blocks": nb, "ms": round(t * 1e3, 3),
                           "MBps": round(n / t / 1e6, 1), "frac": round(ops / t / peak, 4)}), flush=True)
 
 
