@@ -23,7 +23,6 @@
 #include "seg_launch.h"
 #include "analysis.cuh"
 #include "sha256.cuh"
-#include "spectra.cuh"
 #include "stats.cuh"
 
 namespace {
@@ -214,11 +213,12 @@ bool seg_plan(const lz::DevConst& C, uint32_t integrator, lz::SegPlan* P, int* c
     // RK4-FMA, from 3 waves of 16 warps per SM on, where the dynamic CTA dispatch balances the
     // SMs. RK4 keeps the balanced kernel at every larger size (1 GiB: 98.05 % against 97.9 %).
     if (w < 2) return false;
-    if (integrator != LORENZ_RK4 && U > 3 * 16 * sms) return false;
-    // RK4-FMA: the wave kernel runs 20 warps per SM (5 x 128 threads, <= 96 registers), which
-    // its shorter dependent chains need; the balanced kernel's 12-16 reach ~85 %, so it only wins
-    // while the wave kernel's single wave splits badly (C3: 85 % vs 78 %; 128 MiB: 84 % vs 90 %)
-    if (integrator == LORENZ_RK4_FMA && U >= 24 * sms) return false;
+    if (integrator == LORENZ_EULER && U > 3 * 16 * sms) return false;
+    // RK4-FMA: the wave kernel runs 20 warps per SM (5 x 128 threads, <= 96 registers); with its
+    // constants in uniform registers (integrate: no PIN for the FMA form) the balanced kernel
+    // reaches 94.1-94.7 % at 12-16 warps and wins below three such waves (64 MiB 94.1 % vs 80.7 %,
+    // 128 MiB 94.4 vs 92.5, 256 MiB 94.7 vs 94.0; equal at 512 MiB, 94.7 vs 95.0 at 1 GiB)
+    if (integrator == LORENZ_RK4_FMA && U >= 3 * 20 * sms) return false;
     if (U <= 16 * sms) {
       const uint64_t per_smsp_max = 2 * ((((U + 7) / 8) + sms - 1) / sms);
       if (100 * U >= 99 * 4 * sms * per_smsp_max) return false;
@@ -324,7 +324,8 @@ lorenz_status alloc_result(lorenz_result** d_res, cudaStream_t st) {
 }  // namespace
 
 namespace lz {
-void set_last_error(const std::string& s) { g_err = s; }  // shared with lorenz_io.cu
+void set_last_error(const std::string& s) { g_err = s; }  // shared with lorenz_io.cu, lorenz_spectra.cu
+int device_sm_count() { return sm_count(); }             // shared with lorenz_spectra.cu
 
 // The library's own stream-ordered pool, one per device, created on first use. Per-call scratch
 // (result slots, key arrays, hand-over state, FFT workspaces, staged host-path buffers) comes
@@ -832,190 +833,6 @@ lorenz_status lorenz_digit_histograms(const double* ic, uint64_t lanes, uint32_t
   else
     lz::digit_hist_kernel<LORENZ_RK4><<<grid, lz::kCta, 0, st>>>(C, ic, lanes, skip, samples, stride, h);
   return cuda_ok(cudaGetLastError(), "digit_hist") ? LORENZ_OK : LORENZ_E_CUDA;
-}
-
-// ---------------------------------------------------------------- NEXT-4 §4 spectra
-}  // extern "C"
-namespace {
-bool fft_side(uint32_t v) { return v >= 2 && v <= 4096 && (v & (v - 1)) == 0; }
-uint32_t ilog2(uint32_t v) { return 31u - (uint32_t)__builtin_clz(v); }
-
-// workspace row pitch (elements). Padding it (2..256 elements) measured no difference at 4096^2,
-// so the workspace is dense.
-uint64_t fft_ws_pitch(uint32_t W) { return W; }
-
-lz::FftPass fft_rows(uint32_t H, uint32_t W, uint64_t in_pitch, uint64_t out_pitch) {
-  lz::FftPass p = lz::fft_plan(W, ilog2(W), H, true);
-  p.rows = 1;
-  p.in_pitch = in_pitch;
-  p.out_pitch = out_pitch;
-  p.H = H;
-  p.W = W;
-  return p;
-}
-lz::FftPass fft_cols(uint32_t H, uint32_t W, uint64_t in_pitch, uint64_t out_pitch) {
-  lz::FftPass p = lz::fft_plan(H, ilog2(H), W, false);
-  p.rows = 0;
-  p.in_pitch = in_pitch;
-  p.out_pitch = out_pitch;
-  p.H = H;
-  p.W = W;
-  return p;
-}
-
-// one 1-D FFT pass over the batch; n >= 1024 runs the persistent prefetching kernel (complex input,
-// or 16-byte aligned byte rows). *grid_out = the grid used (one flatness partial per CTA).
-template <int IN, int OUT>
-bool fft_launch(const lz::FftPass& p, const uint8_t* bytes, const double2* cin, double2* cout, double* rout,
-                const unsigned long long* sum, double* lag0, cudaStream_t st, unsigned* grid_out = nullptr) {
-  const size_t smem = lz::fft_smem_bytes(
-      p, OUT == lz::FFT_OUT_R2C || OUT == lz::FFT_OUT_HALF_SPECTRUM || OUT == lz::FFT_OUT_POWER_FFT);
-  const unsigned tiles = (p.nseq + p.S - 1) / p.S, cta = lz::fft_cta(p.n, p.rows != 0);
-  const bool persist =
-      p.logn >= 10 && OUT <= lz::FFT_OUT_REAL && IN <= lz::FFT_IN_COMPLEX &&  // plain modes only
-      (IN == lz::FFT_IN_COMPLEX || (p.rows && p.in_pitch == p.n && aligned16(bytes)));
-  auto go = [&](auto kernel) {
-    if (!cuda_ok(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "fft smem"))
-      return false;
-    unsigned grid = tiles;
-    if (persist) {
-      int occ = 0;
-      if (!cuda_ok(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, (int)cta, smem), "fft occupancy"))
-        return false;
-      grid = std::min<unsigned>(tiles, (unsigned)std::max(1, occ) * (unsigned)sm_count());
-    }
-    if (grid_out) *grid_out = grid;
-    kernel<<<grid, cta, smem, st>>>(p, bytes, cin, cout, rout, sum, lag0);
-    return cuda_ok(cudaGetLastError(), "fft pass");
-  };
-  switch (p.logn) {
-    case 1: return go(lz::fft_pass_kernel<IN, OUT, 1, 256>);
-    case 2: return go(lz::fft_pass_kernel<IN, OUT, 2, 256>);
-    case 3: return go(lz::fft_pass_kernel<IN, OUT, 3, 256>);
-    case 4: return go(lz::fft_pass_kernel<IN, OUT, 4, 256>);
-    case 5: return go(lz::fft_pass_kernel<IN, OUT, 5, 256>);
-    case 6: return go(lz::fft_pass_kernel<IN, OUT, 6, 256>);
-    case 7: return go(lz::fft_pass_kernel<IN, OUT, 7, 256>);
-    case 8: return go(lz::fft_pass_kernel<IN, OUT, 8, 256>);
-    case 9: return go(lz::fft_pass_kernel<IN, OUT, 9, 256>);
-    case 10:
-      return persist ? go(lz::fft_persistent_kernel<IN, OUT, 10, 256>) : go(lz::fft_pass_kernel<IN, OUT, 10, 256>);
-    case 11:
-      return persist ? go(lz::fft_persistent_kernel<IN, OUT, 11, 256>) : go(lz::fft_pass_kernel<IN, OUT, 11, 256>);
-    default:
-      if (cta == 512)
-        return persist ? go(lz::fft_persistent_kernel<IN, OUT, 12, 512>) : go(lz::fft_pass_kernel<IN, OUT, 12, 512>);
-      return persist ? go(lz::fft_persistent_kernel<IN, OUT, 12, 256>) : go(lz::fft_pass_kernel<IN, OUT, 12, 256>);
-  }
-}
-
-
-
-lorenz_status spectra_args(const uint8_t* x, uint32_t H, uint32_t W, const double* out) {
-  if (!x || !out || !fft_side(H) || !fft_side(W) || (reinterpret_cast<uintptr_t>(out) & 7)) {
-    g_err = "H and W must be powers of two in [2, 4096]; x and out non-null device pointers, out 8-aligned";
-    return LORENZ_E_ARG;
-  }
-  return LORENZ_OK;
-}
-}  // namespace
-extern "C" {
-
-lorenz_status lorenz_power_spectrum(const uint8_t* x, uint32_t H, uint32_t W, double* power, double* flatness,
-                                    void* stream) {
-  Trace tr("lorenz_power_spectrum");
-  lorenz_status ret = spectra_args(x, H, W, power);
-  if (ret != LORENZ_OK) return ret;
-  cudaStream_t st = (cudaStream_t)stream;
-  const uint64_t N = (uint64_t)H * W;
-  double2* ws = nullptr;
-  double2* part = nullptr;
-  // real input: W-point row transforms as W/2-point complex FFTs of byte pairs (FFT_IN_PAIRS ->
-  // FFT_OUT_R2C), then W/2 packed columns whose powers are written at (k, l) and (-k, -l)
-  // (FFT_OUT_HALF_SPECTRUM): half the FFT work and the workspace of the complex path. W = 2 keeps
-  // the complex path.
-  const bool r2c = W >= 4;
-  const uint32_t M = r2c ? W / 2 : W;
-  const uint64_t NW = (uint64_t)H * M;
-  if (!cuda_ok(lz::lib_malloc_async(reinterpret_cast<void**>(&ws), NW * sizeof(double2), st), "alloc fft"))
-    return LORENZ_E_CUDA;
-  lz::FftPass rows = fft_rows(H, M, W, M), cols = fft_cols(H, M, M, W);
-  rows.W = cols.W = W;
-  cols.scale = std::ldexp(1.0, -2 * (int)ilog2((uint32_t)N));  // 1 / N^2
-  const uint32_t tiles = (cols.nseq + cols.S - 1) / cols.S;  // >= the column pass's grid
-  unsigned nparts = 0;                                          // one flatness partial per column CTA
-  bool ok = !flatness ||
-            cuda_ok(lz::lib_malloc_async(reinterpret_cast<void**>(&part), tiles * sizeof(double2), st), "alloc");
-  cols.part = flatness ? part : nullptr;
-  if (r2c)
-    ok = ok &&
-         fft_launch<lz::FFT_IN_PAIRS, lz::FFT_OUT_R2C>(rows, x, nullptr, ws, nullptr, nullptr, nullptr, st) &&
-         fft_launch<lz::FFT_IN_COMPLEX, lz::FFT_OUT_HALF_SPECTRUM>(cols, nullptr, ws, ws, power, nullptr, nullptr,
-                                                                   st, &nparts);
-  else
-    ok = ok &&
-         fft_launch<lz::FFT_IN_BYTES, lz::FFT_OUT_COMPLEX>(rows, x, nullptr, ws, nullptr, nullptr, nullptr, st) &&
-         fft_launch<lz::FFT_IN_COMPLEX, lz::FFT_OUT_SPECTRUM>(cols, nullptr, ws, ws, power, nullptr, nullptr, st,
-                                                              &nparts);
-  if (ok && flatness) {
-    lz::flatness_final_kernel<<<1, lz::kFftCta, 0, st>>>(part, nparts, N - 1, flatness);
-    ok = cuda_ok(cudaGetLastError(), "flatness");
-  }
-  cudaFreeAsync(ws, st);
-  if (part) cudaFreeAsync(part, st);
-  return ok ? LORENZ_OK : LORENZ_E_CUDA;
-}
-
-lorenz_status lorenz_autocorrelation(const uint8_t* x, uint32_t H, uint32_t W, double* r, void* stream) {
-  Trace tr("lorenz_autocorrelation");
-  lorenz_status ret = spectra_args(x, H, W, r);
-  if (ret != LORENZ_OK) return ret;
-  cudaStream_t st = (cudaStream_t)stream;
-  const uint64_t N = (uint64_t)H * W;
-  double2* ws = nullptr;
-  unsigned long long* aux = nullptr;  // [0] = byte sum, [1] = lag-0 value (double bits)
-  // real input (W >= 4): R2C rows of centred byte pairs -> one fused column pass (transform, |.|^2,
-  // transform: FFT_OUT_POWER_FFT) over the W/2 packed columns -> C2R rows -> normalisation.
-  // Three transform passes over a half-size workspace instead of four full ones; W = 2 keeps the
-  // complex path.
-  const bool r2c = W >= 4;
-  const uint32_t M = r2c ? W / 2 : W;
-  const uint64_t Pw = r2c ? M : fft_ws_pitch(W), NW = (uint64_t)H * Pw;
-  if (!cuda_ok(lz::lib_malloc_async(reinterpret_cast<void**>(&ws), NW * sizeof(double2), st), "alloc fft") ||
-      !cuda_ok(lz::lib_malloc_async(reinterpret_cast<void**>(&aux), 16, st), "alloc aux")) {
-    if (ws) cudaFreeAsync(ws, st);
-    return LORENZ_E_CUDA;
-  }
-  double* lag0 = reinterpret_cast<double*>(aux + 1);
-  const unsigned sgrid = (unsigned)std::min<uint64_t>(4ull * sm_count(), (N + lz::kFftCta - 1) / lz::kFftCta);
-  bool ok = cuda_ok(cudaMemsetAsync(aux, 0, 16, st), "memset");
-  if (ok) {
-    lz::byte_sum_kernel<<<sgrid, lz::kFftCta, 0, st>>>(x, N, aux);
-    ok = cuda_ok(cudaGetLastError(), "byte sum");
-  }
-  if (ok && r2c) {
-    lz::FftPass rows1 = fft_rows(H, M, W, M), cols = fft_cols(H, M, M, M);
-    lz::FftPass rows2 = fft_rows(H, M, M, M);
-    rows1.W = cols.W = rows2.W = W;
-    cols.packed0 = 1;
-    ok = fft_launch<lz::FFT_IN_PAIRS_CENTRED, lz::FFT_OUT_R2C>(rows1, x, nullptr, ws, nullptr, aux, nullptr, st) &&
-         fft_launch<lz::FFT_IN_COMPLEX, lz::FFT_OUT_POWER_FFT>(cols, nullptr, ws, ws, nullptr, nullptr, nullptr, st) &&
-         fft_launch<lz::FFT_IN_C2R, lz::FFT_OUT_REAL_PAIRS>(rows2, nullptr, ws, nullptr, r, nullptr, lag0, st);
-  } else if (ok) {
-    const lz::FftPass rows1 = fft_rows(H, W, W, Pw), cols1 = fft_cols(H, W, Pw, Pw);
-    const lz::FftPass rows2 = fft_rows(H, W, Pw, Pw), cols2 = fft_cols(H, W, Pw, W);
-    ok = fft_launch<lz::FFT_IN_CENTRED, lz::FFT_OUT_COMPLEX>(rows1, x, nullptr, ws, nullptr, aux, nullptr, st) &&
-         fft_launch<lz::FFT_IN_COMPLEX, lz::FFT_OUT_POWER>(cols1, nullptr, ws, ws, nullptr, nullptr, nullptr, st) &&
-         fft_launch<lz::FFT_IN_COMPLEX, lz::FFT_OUT_COMPLEX>(rows2, nullptr, ws, ws, nullptr, nullptr, nullptr, st) &&
-         fft_launch<lz::FFT_IN_COMPLEX, lz::FFT_OUT_REAL>(cols2, nullptr, ws, nullptr, r, nullptr, lag0, st);
-  }
-  if (ok) {
-    lz::autocorr_normalise_kernel<<<sgrid, lz::kFftCta, 0, st>>>(r, N, lag0);
-    ok = cuda_ok(cudaGetLastError(), "normalise");
-  }
-  cudaFreeAsync(ws, st);
-  cudaFreeAsync(aux, st);
-  return ok ? LORENZ_OK : LORENZ_E_CUDA;
 }
 
 // ---------------------------------------------------------------- C5 statistics

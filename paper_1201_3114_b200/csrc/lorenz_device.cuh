@@ -313,10 +313,17 @@ __device__ __forceinline__ void euler_step(double& x, double& y, double& z, doub
 // re-reads them from the constant bank inside the RK4 loop of that kernel's cut-unit paths
 // (3 LDCU.128 per step, 81 instead of 78 instructions); the wave kernel keeps them in uniform
 // registers by itself.
+// Not for the FMA form: its three-operand DFMAs then read the constants from the general register
+// file and lose issue slots to register-bank conflicts; ptxas's per-step reload of the constants
+// into uniform registers (3 LDCU.128, off the FP64 pipe) costs far less (C3 in the balanced kernel:
+// 85.3 % -> 94.4 % of the FP64 pipe, tools/tune.py). Bit i of LZ_PIN_MASK pins integrator i.
+#ifndef LZ_PIN_MASK
+#define LZ_PIN_MASK 3
+#endif
 template <int INTEG, bool PIN = false>
 __device__ __forceinline__ void integrate(double& x, double& y, double& z, const DevConst& C) {
   double S = C.sigma, R = C.rho, Bt = C.beta, h = C.h, h2 = C.h2, h6 = C.h6;
-  if (PIN) {
+  if (PIN && ((LZ_PIN_MASK >> INTEG) & 1)) {
     asm volatile("add.rn.f64 %0, %0, 0d0000000000000000;" : "+d"(S));
     asm volatile("add.rn.f64 %0, %0, 0d0000000000000000;" : "+d"(R));
     asm volatile("add.rn.f64 %0, %0, 0d0000000000000000;" : "+d"(Bt));

@@ -1,0 +1,258 @@
+// lorenz_spectra.cu — host side of the NEXT-4 analysis calls lorenz_power_spectrum and
+// lorenz_autocorrelation (include/lorenz.h): the FFT pass plans and launches of spectra.cuh
+// (single-CTA passes) and spectra_cluster.cuh (the 4-CTA cluster column pass). A translation
+// unit of its own so the FFT instantiations compile beside the chain kernels (build.py).
+#include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <string>
+
+#include "../../include/lorenz.h"
+#include "seg_launch.h"
+#include "spectra.cuh"
+#include "spectra_cluster.cuh"
+
+namespace lz {
+void set_last_error(const std::string& s);  // lorenz.cu
+int device_sm_count();                      // lorenz.cu
+}  // namespace lz
+
+namespace {
+bool cuda_ok(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return true;
+  lz::set_last_error(std::string(what) + ": " + cudaGetErrorString(e));
+  return false;
+}
+int sm_count() { return lz::device_sm_count(); }
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+struct Trace {
+  explicit Trace(const char* name) { nvtxRangePushA(name); }
+  ~Trace() { nvtxRangePop(); }
+};
+}  // namespace
+
+namespace {
+bool fft_side(uint32_t v) { return v >= 2 && v <= 4096 && (v & (v - 1)) == 0; }
+uint32_t ilog2(uint32_t v) { return 31u - (uint32_t)__builtin_clz(v); }
+
+// workspace row pitch (elements). Padding it (2..256 elements) measured no difference at 4096^2,
+// so the workspace is dense.
+uint64_t fft_ws_pitch(uint32_t W) { return W; }
+
+lz::FftPass fft_rows(uint32_t H, uint32_t W, uint64_t in_pitch, uint64_t out_pitch) {
+  lz::FftPass p = lz::fft_plan(W, ilog2(W), H, true);
+  p.rows = 1;
+  p.in_pitch = in_pitch;
+  p.out_pitch = out_pitch;
+  p.H = H;
+  p.W = W;
+  return p;
+}
+lz::FftPass fft_cols(uint32_t H, uint32_t W, uint64_t in_pitch, uint64_t out_pitch) {
+  lz::FftPass p = lz::fft_plan(H, ilog2(H), W, false);
+  p.rows = 0;
+  p.in_pitch = in_pitch;
+  p.out_pitch = out_pitch;
+  p.H = H;
+  p.W = W;
+  return p;
+}
+
+// one 1-D FFT pass over the batch; n >= 1024 runs the persistent prefetching kernel (complex input,
+// or 16-byte aligned byte rows). *grid_out = the grid used (one flatness partial per CTA).
+template <int IN, int OUT>
+bool fft_launch(const lz::FftPass& p, const uint8_t* bytes, const double2* cin, double2* cout, double* rout,
+                const unsigned long long* sum, double* lag0, cudaStream_t st, unsigned* grid_out = nullptr) {
+  const size_t smem = lz::fft_smem_bytes(
+      p, OUT == lz::FFT_OUT_R2C || OUT == lz::FFT_OUT_HALF_SPECTRUM || OUT == lz::FFT_OUT_POWER_FFT);
+  const unsigned tiles = (p.nseq + p.S - 1) / p.S, cta = lz::fft_cta(p.n, p.rows != 0);
+  const bool persist =
+      p.logn >= 10 && OUT <= lz::FFT_OUT_REAL && IN <= lz::FFT_IN_COMPLEX &&  // plain modes only
+      (IN == lz::FFT_IN_COMPLEX || (p.rows && p.in_pitch == p.n && aligned16(bytes)));
+  auto go = [&](auto kernel) {
+    if (!cuda_ok(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "fft smem"))
+      return false;
+    unsigned grid = tiles;
+    if (persist) {
+      int occ = 0;
+      if (!cuda_ok(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, (int)cta, smem), "fft occupancy"))
+        return false;
+      grid = std::min<unsigned>(tiles, (unsigned)std::max(1, occ) * (unsigned)sm_count());
+    }
+    if (grid_out) *grid_out = grid;
+    kernel<<<grid, cta, smem, st>>>(p, bytes, cin, cout, rout, sum, lag0);
+    return cuda_ok(cudaGetLastError(), "fft pass");
+  };
+  switch (p.logn) {
+    case 1: return go(lz::fft_pass_kernel<IN, OUT, 1, 256>);
+    case 2: return go(lz::fft_pass_kernel<IN, OUT, 2, 256>);
+    case 3: return go(lz::fft_pass_kernel<IN, OUT, 3, 256>);
+    case 4: return go(lz::fft_pass_kernel<IN, OUT, 4, 256>);
+    case 5: return go(lz::fft_pass_kernel<IN, OUT, 5, 256>);
+    case 6: return go(lz::fft_pass_kernel<IN, OUT, 6, 256>);
+    case 7: return go(lz::fft_pass_kernel<IN, OUT, 7, 256>);
+    case 8: return go(lz::fft_pass_kernel<IN, OUT, 8, 256>);
+    case 9: return go(lz::fft_pass_kernel<IN, OUT, 9, 256>);
+    case 10:
+      return persist ? go(lz::fft_persistent_kernel<IN, OUT, 10, 256>) : go(lz::fft_pass_kernel<IN, OUT, 10, 256>);
+    case 11:
+      return persist ? go(lz::fft_persistent_kernel<IN, OUT, 11, 256>) : go(lz::fft_pass_kernel<IN, OUT, 11, 256>);
+    default:
+      if (cta == 512)
+        return persist ? go(lz::fft_persistent_kernel<IN, OUT, 12, 512>) : go(lz::fft_pass_kernel<IN, OUT, 12, 512>);
+      return persist ? go(lz::fft_persistent_kernel<IN, OUT, 12, 256>) : go(lz::fft_pass_kernel<IN, OUT, 12, 256>);
+  }
+}
+
+
+
+// The cluster column pass (spectra_cluster.cuh) for H = 2048 and 4096: four CTAs per group of 8
+// adjacent packed columns, 128-byte row segments. *grid_out = its grid (one flatness partial per CTA).
+constexpr uint32_t kClusterCols = 8;
+bool use_cluster_cols(uint32_t H, uint32_t M) { return (H == 4096 || H == 2048) && M >= kClusterCols; }
+
+template <int OUT>
+bool fft_cluster_launch(uint32_t H, uint32_t W, uint32_t M, double scale, uint32_t packed0, double2* part,
+                        const double2* cin, double2* cout, double* rout, cudaStream_t st, unsigned* grid_out) {
+  lz::FftPass c = lz::fft_plan_cluster(H / 4, ilog2(H) - 2, M, kClusterCols);
+  c.rows = 0;
+  c.in_pitch = M;
+  c.out_pitch = M;
+  c.H = H;
+  c.W = W;
+  c.scale = scale;
+  c.packed0 = packed0;
+  c.part = part;
+  const size_t smem = lz::fft_cluster_smem_bytes(c);
+  const unsigned grid = lz::kClusterRanks * (M / kClusterCols);
+  if (grid_out) *grid_out = grid;
+  auto go = [&](auto kernel, unsigned cta) {
+    if (!cuda_ok(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "fft smem"))
+      return false;
+    kernel<<<grid, cta, smem, st>>>(c, cin, cout, rout);
+    return cuda_ok(cudaGetLastError(), "fft cluster pass");
+  };
+  if (H == 4096) return go(lz::fft_col_cluster_kernel<OUT, 12, kClusterCols>, kClusterCols * 1024 / 16);
+  return go(lz::fft_col_cluster_kernel<OUT, 11, kClusterCols>, kClusterCols * 512 / 16);
+}
+
+lorenz_status spectra_args(const uint8_t* x, uint32_t H, uint32_t W, const double* out) {
+  if (!x || !out || !fft_side(H) || !fft_side(W) || (reinterpret_cast<uintptr_t>(out) & 7)) {
+    lz::set_last_error("H and W must be powers of two in [2, 4096]; x and out non-null device pointers, out 8-aligned");
+    return LORENZ_E_ARG;
+  }
+  return LORENZ_OK;
+}
+}  // namespace
+extern "C" {
+
+lorenz_status lorenz_power_spectrum(const uint8_t* x, uint32_t H, uint32_t W, double* power, double* flatness,
+                                    void* stream) {
+  Trace tr("lorenz_power_spectrum");
+  lorenz_status ret = spectra_args(x, H, W, power);
+  if (ret != LORENZ_OK) return ret;
+  cudaStream_t st = (cudaStream_t)stream;
+  const uint64_t N = (uint64_t)H * W;
+  double2* ws = nullptr;
+  double2* part = nullptr;
+  // real input: W-point row transforms as W/2-point complex FFTs of byte pairs (FFT_IN_PAIRS ->
+  // FFT_OUT_R2C), then W/2 packed columns whose powers are written at (k, l) and (-k, -l)
+  // (FFT_OUT_HALF_SPECTRUM): half the FFT work and the workspace of the complex path. W = 2 keeps
+  // the complex path.
+  const bool r2c = W >= 4;
+  const uint32_t M = r2c ? W / 2 : W;
+  const uint64_t NW = (uint64_t)H * M;
+  if (!cuda_ok(lz::lib_malloc_async(reinterpret_cast<void**>(&ws), NW * sizeof(double2), st), "alloc fft"))
+    return LORENZ_E_CUDA;
+  lz::FftPass rows = fft_rows(H, M, W, M), cols = fft_cols(H, M, M, W);
+  rows.W = cols.W = W;
+  cols.scale = std::ldexp(1.0, -2 * (int)ilog2((uint32_t)N));  // 1 / N^2
+  const bool clus = r2c && use_cluster_cols(H, M);
+  const uint32_t tiles = clus ? lz::kClusterRanks * (M / kClusterCols)  // the column pass's grid (or more)
+                              : (cols.nseq + cols.S - 1) / cols.S;
+  unsigned nparts = 0;                                          // one flatness partial per column CTA
+  bool ok = !flatness ||
+            cuda_ok(lz::lib_malloc_async(reinterpret_cast<void**>(&part), tiles * sizeof(double2), st), "alloc");
+  cols.part = flatness ? part : nullptr;
+  if (clus)
+    ok = ok &&
+         fft_launch<lz::FFT_IN_PAIRS, lz::FFT_OUT_R2C>(rows, x, nullptr, ws, nullptr, nullptr, nullptr, st) &&
+         fft_cluster_launch<lz::FFT_OUT_HALF_SPECTRUM>(H, W, M, cols.scale, 0, cols.part, ws, ws, power, st, &nparts);
+  else if (r2c)
+    ok = ok &&
+         fft_launch<lz::FFT_IN_PAIRS, lz::FFT_OUT_R2C>(rows, x, nullptr, ws, nullptr, nullptr, nullptr, st) &&
+         fft_launch<lz::FFT_IN_COMPLEX, lz::FFT_OUT_HALF_SPECTRUM>(cols, nullptr, ws, ws, power, nullptr, nullptr,
+                                                                   st, &nparts);
+  else
+    ok = ok &&
+         fft_launch<lz::FFT_IN_BYTES, lz::FFT_OUT_COMPLEX>(rows, x, nullptr, ws, nullptr, nullptr, nullptr, st) &&
+         fft_launch<lz::FFT_IN_COMPLEX, lz::FFT_OUT_SPECTRUM>(cols, nullptr, ws, ws, power, nullptr, nullptr, st,
+                                                              &nparts);
+  if (ok && flatness) {
+    lz::flatness_final_kernel<<<1, lz::kFftCta, 0, st>>>(part, nparts, N - 1, flatness);
+    ok = cuda_ok(cudaGetLastError(), "flatness");
+  }
+  cudaFreeAsync(ws, st);
+  if (part) cudaFreeAsync(part, st);
+  return ok ? LORENZ_OK : LORENZ_E_CUDA;
+}
+
+lorenz_status lorenz_autocorrelation(const uint8_t* x, uint32_t H, uint32_t W, double* r, void* stream) {
+  Trace tr("lorenz_autocorrelation");
+  lorenz_status ret = spectra_args(x, H, W, r);
+  if (ret != LORENZ_OK) return ret;
+  cudaStream_t st = (cudaStream_t)stream;
+  const uint64_t N = (uint64_t)H * W;
+  double2* ws = nullptr;
+  unsigned long long* aux = nullptr;  // [0] = byte sum, [1] = lag-0 value (double bits)
+  // real input (W >= 4): R2C rows of centred byte pairs -> one fused column pass (transform, |.|^2,
+  // transform: FFT_OUT_POWER_FFT) over the W/2 packed columns -> C2R rows -> normalisation.
+  // Three transform passes over a half-size workspace instead of four full ones; W = 2 keeps the
+  // complex path.
+  const bool r2c = W >= 4;
+  const uint32_t M = r2c ? W / 2 : W;
+  const uint64_t Pw = r2c ? M : fft_ws_pitch(W), NW = (uint64_t)H * Pw;
+  if (!cuda_ok(lz::lib_malloc_async(reinterpret_cast<void**>(&ws), NW * sizeof(double2), st), "alloc fft") ||
+      !cuda_ok(lz::lib_malloc_async(reinterpret_cast<void**>(&aux), 16, st), "alloc aux")) {
+    if (ws) cudaFreeAsync(ws, st);
+    return LORENZ_E_CUDA;
+  }
+  double* lag0 = reinterpret_cast<double*>(aux + 1);
+  const unsigned sgrid = (unsigned)std::min<uint64_t>(4ull * sm_count(), (N + lz::kFftCta - 1) / lz::kFftCta);
+  bool ok = cuda_ok(cudaMemsetAsync(aux, 0, 16, st), "memset");
+  if (ok) {
+    lz::byte_sum_kernel<<<sgrid, lz::kFftCta, 0, st>>>(x, N, aux);
+    ok = cuda_ok(cudaGetLastError(), "byte sum");
+  }
+  if (ok && r2c) {
+    lz::FftPass rows1 = fft_rows(H, M, W, M), cols = fft_cols(H, M, M, M);
+    lz::FftPass rows2 = fft_rows(H, M, M, M);
+    rows1.W = cols.W = rows2.W = W;
+    cols.packed0 = 1;
+    ok = fft_launch<lz::FFT_IN_PAIRS_CENTRED, lz::FFT_OUT_R2C>(rows1, x, nullptr, ws, nullptr, aux, nullptr, st) &&
+         (use_cluster_cols(H, M)
+              ? fft_cluster_launch<lz::FFT_OUT_POWER_FFT>(H, W, M, 1.0, 1, nullptr, ws, ws, nullptr, st, nullptr)
+              : fft_launch<lz::FFT_IN_COMPLEX, lz::FFT_OUT_POWER_FFT>(cols, nullptr, ws, ws, nullptr, nullptr,
+                                                                      nullptr, st)) &&
+         fft_launch<lz::FFT_IN_C2R, lz::FFT_OUT_REAL_PAIRS>(rows2, nullptr, ws, nullptr, r, nullptr, lag0, st);
+  } else if (ok) {
+    const lz::FftPass rows1 = fft_rows(H, W, W, Pw), cols1 = fft_cols(H, W, Pw, Pw);
+    const lz::FftPass rows2 = fft_rows(H, W, Pw, Pw), cols2 = fft_cols(H, W, Pw, W);
+    ok = fft_launch<lz::FFT_IN_CENTRED, lz::FFT_OUT_COMPLEX>(rows1, x, nullptr, ws, nullptr, aux, nullptr, st) &&
+         fft_launch<lz::FFT_IN_COMPLEX, lz::FFT_OUT_POWER>(cols1, nullptr, ws, ws, nullptr, nullptr, nullptr, st) &&
+         fft_launch<lz::FFT_IN_COMPLEX, lz::FFT_OUT_COMPLEX>(rows2, nullptr, ws, ws, nullptr, nullptr, nullptr, st) &&
+         fft_launch<lz::FFT_IN_COMPLEX, lz::FFT_OUT_REAL>(cols2, nullptr, ws, nullptr, r, nullptr, lag0, st);
+  }
+  if (ok) {
+    lz::autocorr_normalise_kernel<<<sgrid, lz::kFftCta, 0, st>>>(r, N, lag0);
+    ok = cuda_ok(cudaGetLastError(), "normalise");
+  }
+  cudaFreeAsync(ws, st);
+  cudaFreeAsync(aux, st);
+  return ok ? LORENZ_OK : LORENZ_E_CUDA;
+}
+
+}  // extern "C"

@@ -41,7 +41,8 @@ enum FftIn : int {
 // FFT_OUT_REAL_PAIRS: the C2R row output R[m] -> real samples (2m, 2m+1) = (Re R, -Im R).
 enum FftOut : int {
   FFT_OUT_COMPLEX = 0, FFT_OUT_POWER = 1, FFT_OUT_SPECTRUM = 2, FFT_OUT_REAL = 3,
-  FFT_OUT_R2C = 4, FFT_OUT_HALF_SPECTRUM = 5, FFT_OUT_POWER_FFT = 6, FFT_OUT_REAL_PAIRS = 7
+  FFT_OUT_R2C = 4, FFT_OUT_HALF_SPECTRUM = 5, FFT_OUT_POWER_FFT = 6, FFT_OUT_REAL_PAIRS = 7,
+  FFT_OUT_SMEM = 8  // the result stays in the shared-memory tile (natural order): the cluster column pass
 };
 
 struct FftPass {
@@ -59,6 +60,8 @@ struct FftPass {
   double scale;         // FFT_OUT_SPECTRUM: 1 / (HW)^2 (a power of two: exact)
   uint32_t packed0;     // FFT_OUT_POWER_FFT: sequence 0 holds the packed DC + i Nyquist column
   double2* part;        // FFT_OUT_SPECTRUM (nullable): per-CTA (sum log P, sum P) over non-DC bins
+  uint32_t kmul, kadd;  // columns: output position pos is row pos * kmul + kadd (1, 0; the cluster
+                        // column pass's CTA r holds rows r + 4 pos)
 };
 
 // CTA threads: 256, except 512 for 4096-point column passes (S = 2 adjacent columns per CTA,
@@ -81,6 +84,8 @@ inline FftPass fft_plan(uint32_t n, uint32_t logn, uint32_t nseq, bool rows) {
   const uint32_t k = rows ? (p.T >= 8 ? 1 : 8 / p.T) : (p.S < 8 ? p.S : 8);
   p.pitch = n + n / 16;
   if (k > 1) p.pitch += ((8 / k) - p.pitch % 8 + 8) % 8;  // pitch = 8/k (mod 8)
+  p.kmul = 1;
+  p.kadd = 0;
   p.npass = 0;
   uint32_t L = logn;
   while (L >= 4) { p.rlog[p.npass++] = 4; L -= 4; }
@@ -242,7 +247,7 @@ __device__ __forceinline__ double2 fft_load(const FftPass& p, const FftIo& io, u
 template <int OUT>
 __device__ __forceinline__ void fft_store(const FftPass& p, const FftIo& io, uint64_t seq, uint32_t pos, double2 v,
                                           FlatAcc& acc) {
-  const uint64_t i = p.rows ? seq : pos, j = p.rows ? pos : seq;  // (row, column) of the element
+  const uint64_t i = p.rows ? seq : (uint64_t)pos * p.kmul + p.kadd, j = p.rows ? pos : seq;  // (row, column)
   if (OUT == FFT_OUT_COMPLEX) {
     io.cout[i * p.out_pitch + j] = v;
   } else if (OUT == FFT_OUT_POWER) {
@@ -319,14 +324,16 @@ __device__ __forceinline__ void fft_pass(const FftPass& p, const FftIo& io, doub
     for (int u = 0; u < R; ++u) {
       const uint32_t pos = (j - k) * R + k + u * LS;
       const double2 v = a[g * R + bitrev_c<R>(u)];
-      if (LAST && !(OUT == FFT_OUT_R2C || OUT == FFT_OUT_POWER_FFT || (OUT == FFT_OUT_HALF_SPECTRUM && seq == 0))) {
+      if (LAST && !(OUT == FFT_OUT_R2C || OUT == FFT_OUT_POWER_FFT || OUT == FFT_OUT_SMEM ||
+                    (OUT == FFT_OUT_HALF_SPECTRUM && seq == 0))) {
         if (valid) fft_store<OUT>(p, io, seq, pos, v, acc);
       } else {
         Xs[fft_pad(pos)] = v;  // exchange, or the input of a shared-memory epilogue
       }
     }
   }
-  if (!LAST || OUT == FFT_OUT_R2C || OUT == FFT_OUT_HALF_SPECTRUM || OUT == FFT_OUT_POWER_FFT) __syncthreads();
+  if (!LAST || OUT == FFT_OUT_R2C || OUT == FFT_OUT_HALF_SPECTRUM || OUT == FFT_OUT_POWER_FFT || OUT == FFT_OUT_SMEM)
+    __syncthreads();
 }
 
 // the passes of an N = 2^LOGN transform: radix 16 while >= 4 bits remain, then the remainder

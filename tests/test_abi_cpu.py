@@ -127,6 +127,8 @@ def test_launch_plan_rules(L, tune):
     assert L.lorenz_launch_plan(key, 0, 0, 1)["lanes"] == 1
     fma = L.lorenz_keysetup(b"0123456789abcdef", mode=L.FAST, integrator=L.RK4_FMA)
     assert L.lorenz_launch_plan(fma, 65536 * 1024, 0, 65536)["kind"] == "balanced"
+    for blocks, kind in ((131072, "balanced"), (262144, "balanced"), (524288, "wave"), (1 << 20, "wave")):
+        assert L.lorenz_launch_plan(fma, blocks * 1024, 0, blocks)["kind"] == kind, blocks  # 3 x 20 warps/SM
     tune(schedule="wave")
     assert plan(65536)["kind"] == "wave"
     tune(schedule="seg", seg_slots=3)

@@ -157,3 +157,39 @@ def test_bad_shapes_rejected(h, w):
     assert st == L.E_ARG
     st = L.lib().lorenz_autocorrelation(x.data_ptr(), h, w, out.data_ptr(), None)
     assert st == L.E_ARG
+
+
+@pytest.mark.parametrize("h,w", [(2048, 16), (2048, 32)])
+def test_cluster_column_pass_full_matrices(h, w):
+    """H = 2048 / 4096 take the 4-CTA cluster column pass (spectra_cluster.cuh: four-step DIF /
+    DIT split across the cluster's shared memories, the packed DC / Nyquist column paired across
+    CTAs). Full matrices against the oracle's plain sums, at H = 2048 (M = 512 rows per CTA)."""
+    x = cipher_image(h, w, seed=h + w)
+    p, f = gpu_spectrum(x)
+    want = oracle.power_spectrum(x)
+    assert np.abs(p - want).max() <= tol_power(x)
+    assert abs(f - oracle.spectral_flatness(want)) <= 1e-9
+    r = gpu_autocorr(x)
+    assert np.abs(r - oracle.autocorr(x)).max() <= tol_autocorr(x.size)
+
+
+@pytest.mark.parametrize("h,w", [(4096, 16), (4096, 64), (2048, 128)])
+def test_cluster_column_pass_sampled(h, w):
+    """H = 4096 (M = 1024 rows per CTA) and a wider H = 2048 matrix: every residue class k mod 4,
+    the packed column's DC / Nyquist outputs (l = 0, W/2) and their neighbours, against the oracle
+    one frequency / lag at a time; Parseval and r(0,0) = 1 over the whole matrix."""
+    x = cipher_image(h, w, seed=h ^ w)
+    p, _ = gpu_spectrum(x)
+    r = gpu_autocorr(x)
+    rng = np.random.default_rng(h + w)
+    ks = [0, 1, 2, 3, 4, 5, h // 2 - 1, h // 2, h // 2 + 1, h - 4, h - 3, h - 2, h - 1] + list(rng.integers(0, h, 8))
+    ls = [0, 1, w // 2 - 1, w // 2, w // 2 + 1, w - 1] + list(rng.integers(0, w, 2))
+    for k in ks:
+        for l in ls:
+            got = p[(k + h // 2) % h, (l + w // 2) % w]
+            assert abs(got - oracle.power_at(x, int(k), int(l))) <= tol_power(x), (k, l)
+    for k in ks[::2]:
+        for l in ls[::2]:
+            assert abs(r[k, l] - oracle.autocorr_at(x, int(k), int(l))) <= tol_autocorr(x.size), (k, l)
+    assert math.isclose(p.sum(), float((x.astype(np.float64) ** 2).mean()), rel_tol=1e-11)
+    assert r[0, 0] == pytest.approx(1.0, abs=1e-13)
