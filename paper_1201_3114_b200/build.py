@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(CSRC, "liblorenz.so")
 SOURCES = ["lorenz.cu", "lorenz_io.cu", "lorenz_seg.cu", "lorenz_spectra.cu"]
-HEADERS = ["lorenz_device.cuh", "sha256.cuh", "stats.cuh", "analysis.cuh", "spectra.cuh", "spectra_cluster.cuh", "seg_launch.h",
+HEADERS = ["lorenz_device.cuh", "sha256.cuh", "stats.cuh", "analysis.cuh", "spectra.cuh", "seg_launch.h",
            os.path.join("..", "..", "include", "lorenz.h")]
 # translation units, compiled in parallel: lorenz_seg.cu once per OP (its kernel instantiations
 # are the bulk of the compile time)

@@ -1,7 +1,7 @@
 // lorenz_spectra.cu — host side of the NEXT-4 analysis calls lorenz_power_spectrum and
-// lorenz_autocorrelation (include/lorenz.h): the FFT pass plans and launches of spectra.cuh
-// (single-CTA passes) and spectra_cluster.cuh (the 4-CTA cluster column pass). A translation
-// unit of its own so the FFT instantiations compile beside the chain kernels (build.py).
+// lorenz_autocorrelation (include/lorenz.h): the FFT pass plans and launches of spectra.cuh.
+// A translation unit of its own so the FFT instantiations compile beside the chain kernels
+// (build.py).
 #include <cuda_runtime.h>
 #include <nvtx3/nvToolsExt.h>
 
@@ -13,7 +13,6 @@
 #include "../../include/lorenz.h"
 #include "seg_launch.h"
 #include "spectra.cuh"
-#include "spectra_cluster.cuh"
 
 namespace lz {
 void set_last_error(const std::string& s);  // lorenz.cu
@@ -109,36 +108,6 @@ bool fft_launch(const lz::FftPass& p, const uint8_t* bytes, const double2* cin, 
 
 
 
-// The cluster column pass (spectra_cluster.cuh) for H = 2048 and 4096: four CTAs per group of 8
-// adjacent packed columns, 128-byte row segments. *grid_out = its grid (one flatness partial per CTA).
-constexpr uint32_t kClusterCols = 8;
-bool use_cluster_cols(uint32_t H, uint32_t M) { return (H == 4096 || H == 2048) && M >= kClusterCols; }
-
-template <int OUT>
-bool fft_cluster_launch(uint32_t H, uint32_t W, uint32_t M, double scale, uint32_t packed0, double2* part,
-                        const double2* cin, double2* cout, double* rout, cudaStream_t st, unsigned* grid_out) {
-  lz::FftPass c = lz::fft_plan_cluster(H / 4, ilog2(H) - 2, M, kClusterCols);
-  c.rows = 0;
-  c.in_pitch = M;
-  c.out_pitch = M;
-  c.H = H;
-  c.W = W;
-  c.scale = scale;
-  c.packed0 = packed0;
-  c.part = part;
-  const size_t smem = lz::fft_cluster_smem_bytes(c);
-  const unsigned grid = lz::kClusterRanks * (M / kClusterCols);
-  if (grid_out) *grid_out = grid;
-  auto go = [&](auto kernel, unsigned cta) {
-    if (!cuda_ok(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "fft smem"))
-      return false;
-    kernel<<<grid, cta, smem, st>>>(c, cin, cout, rout);
-    return cuda_ok(cudaGetLastError(), "fft cluster pass");
-  };
-  if (H == 4096) return go(lz::fft_col_cluster_kernel<OUT, 12, kClusterCols>, kClusterCols * 1024 / 16);
-  return go(lz::fft_col_cluster_kernel<OUT, 11, kClusterCols>, kClusterCols * 512 / 16);
-}
-
 lorenz_status spectra_args(const uint8_t* x, uint32_t H, uint32_t W, const double* out) {
   if (!x || !out || !fft_side(H) || !fft_side(W) || (reinterpret_cast<uintptr_t>(out) & 7)) {
     lz::set_last_error("H and W must be powers of two in [2, 4096]; x and out non-null device pointers, out 8-aligned");
@@ -170,18 +139,12 @@ lorenz_status lorenz_power_spectrum(const uint8_t* x, uint32_t H, uint32_t W, do
   lz::FftPass rows = fft_rows(H, M, W, M), cols = fft_cols(H, M, M, W);
   rows.W = cols.W = W;
   cols.scale = std::ldexp(1.0, -2 * (int)ilog2((uint32_t)N));  // 1 / N^2
-  const bool clus = r2c && use_cluster_cols(H, M);
-  const uint32_t tiles = clus ? lz::kClusterRanks * (M / kClusterCols)  // the column pass's grid (or more)
-                              : (cols.nseq + cols.S - 1) / cols.S;
+  const uint32_t tiles = (cols.nseq + cols.S - 1) / cols.S;  // >= the column pass's grid
   unsigned nparts = 0;                                          // one flatness partial per column CTA
   bool ok = !flatness ||
             cuda_ok(lz::lib_malloc_async(reinterpret_cast<void**>(&part), tiles * sizeof(double2), st), "alloc");
   cols.part = flatness ? part : nullptr;
-  if (clus)
-    ok = ok &&
-         fft_launch<lz::FFT_IN_PAIRS, lz::FFT_OUT_R2C>(rows, x, nullptr, ws, nullptr, nullptr, nullptr, st) &&
-         fft_cluster_launch<lz::FFT_OUT_HALF_SPECTRUM>(H, W, M, cols.scale, 0, cols.part, ws, ws, power, st, &nparts);
-  else if (r2c)
+  if (r2c)
     ok = ok &&
          fft_launch<lz::FFT_IN_PAIRS, lz::FFT_OUT_R2C>(rows, x, nullptr, ws, nullptr, nullptr, nullptr, st) &&
          fft_launch<lz::FFT_IN_COMPLEX, lz::FFT_OUT_HALF_SPECTRUM>(cols, nullptr, ws, ws, power, nullptr, nullptr,
@@ -233,10 +196,7 @@ lorenz_status lorenz_autocorrelation(const uint8_t* x, uint32_t H, uint32_t W, d
     rows1.W = cols.W = rows2.W = W;
     cols.packed0 = 1;
     ok = fft_launch<lz::FFT_IN_PAIRS_CENTRED, lz::FFT_OUT_R2C>(rows1, x, nullptr, ws, nullptr, aux, nullptr, st) &&
-         (use_cluster_cols(H, M)
-              ? fft_cluster_launch<lz::FFT_OUT_POWER_FFT>(H, W, M, 1.0, 1, nullptr, ws, ws, nullptr, st, nullptr)
-              : fft_launch<lz::FFT_IN_COMPLEX, lz::FFT_OUT_POWER_FFT>(cols, nullptr, ws, ws, nullptr, nullptr,
-                                                                      nullptr, st)) &&
+         fft_launch<lz::FFT_IN_COMPLEX, lz::FFT_OUT_POWER_FFT>(cols, nullptr, ws, ws, nullptr, nullptr, nullptr, st) &&
          fft_launch<lz::FFT_IN_C2R, lz::FFT_OUT_REAL_PAIRS>(rows2, nullptr, ws, nullptr, r, nullptr, lag0, st);
   } else if (ok) {
     const lz::FftPass rows1 = fft_rows(H, W, W, Pw), cols1 = fft_cols(H, W, Pw, Pw);

@@ -160,10 +160,9 @@ def test_bad_shapes_rejected(h, w):
 
 
 @pytest.mark.parametrize("h,w", [(2048, 16), (2048, 32)])
-def test_cluster_column_pass_full_matrices(h, w):
-    """H = 2048 / 4096 take the 4-CTA cluster column pass (spectra_cluster.cuh: four-step DIF /
-    DIT split across the cluster's shared memories, the packed DC / Nyquist column paired across
-    CTAs). Full matrices against the oracle's plain sums, at H = 2048 (M = 512 rows per CTA)."""
+def test_tall_matrices_full(h, w):
+    """Tall matrices (2048-point column transforms over 8-16 packed columns, the packed DC /
+    Nyquist column included): full matrices against the oracle's plain sums."""
     x = cipher_image(h, w, seed=h + w)
     p, f = gpu_spectrum(x)
     want = oracle.power_spectrum(x)
@@ -174,10 +173,10 @@ def test_cluster_column_pass_full_matrices(h, w):
 
 
 @pytest.mark.parametrize("h,w", [(4096, 16), (4096, 64), (2048, 128)])
-def test_cluster_column_pass_sampled(h, w):
-    """H = 4096 (M = 1024 rows per CTA) and a wider H = 2048 matrix: every residue class k mod 4,
-    the packed column's DC / Nyquist outputs (l = 0, W/2) and their neighbours, against the oracle
-    one frequency / lag at a time; Parseval and r(0,0) = 1 over the whole matrix."""
+def test_tall_matrices_sampled(h, w):
+    """4096- and 2048-point column transforms: frequencies in every residue class k mod 4 and at
+    both ends, the packed column's DC / Nyquist outputs (l = 0, W/2) and their neighbours, against
+    the oracle one frequency / lag at a time; Parseval and r(0,0) = 1 over the whole matrix."""
     x = cipher_image(h, w, seed=h ^ w)
     p, _ = gpu_spectrum(x)
     r = gpu_autocorr(x)
