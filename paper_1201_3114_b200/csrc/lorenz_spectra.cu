@@ -108,6 +108,55 @@ bool fft_launch(const lz::FftPass& p, const uint8_t* bytes, const double2* cin, 
 
 
 
+// The four-step column transform of the power spectrum (spectra.cuh "four-step column transform"):
+// H = 16 H2 for H = 2048, 4096, with at least 8 packed columns.
+bool four_step_cols(uint32_t H, uint32_t M) { return (H == 2048 || H == 4096) && M >= 8; }
+
+lz::FftPass four_step_stage2(uint32_t H, uint32_t W, uint32_t M) {
+  const uint32_t H2 = H / 16;
+  lz::FftPass c = lz::fft_plan(H2, ilog2(H2), M, false);
+  c.rows = 0;
+  c.in_pitch = M;
+  c.out_pitch = M;
+  c.H = H;
+  c.W = W;
+  c.kmul = 16;
+  c.ysplit = 1;
+  c.in_y_off = (uint64_t)H2 * M;
+  return c;
+}
+
+// stage 1 -> stage 2 (16 blocks of H2 rows) -> the packed column's unpacking; *nparts = flatness
+// partials written (stage 2's CTAs, then the unpacking's one)
+bool four_step_spectrum(uint32_t H, uint32_t W, uint32_t M, double scale, double2* ws, double2* col0,
+                        double* power, double2* part, cudaStream_t st, unsigned* nparts) {
+  const uint32_t H2 = H / 16;
+  lz::FftPass c = four_step_stage2(H, W, M);
+  c.scale = scale;
+  c.part = part;
+  c.col0_out = col0;
+  lz::FftPass s1 = c;
+  const dim3 g1(H2 / 32, (M + 7) / 8);
+  if (H == 4096) lz::fft_col_stage1_kernel<12><<<g1, 256, 0, st>>>(s1, ws);
+  else lz::fft_col_stage1_kernel<11><<<g1, 256, 0, st>>>(s1, ws);
+  if (!cuda_ok(cudaGetLastError(), "fft stage 1")) return false;
+  const size_t smem = lz::fft_smem_bytes(c, true);
+  const dim3 g2((c.nseq + c.S - 1) / c.S, 16);
+  auto go = [&](auto kernel) {
+    if (!cuda_ok(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "fft smem"))
+      return false;
+    kernel<<<g2, 256, smem, st>>>(c, nullptr, ws, nullptr, power, nullptr, nullptr);
+    return cuda_ok(cudaGetLastError(), "fft stage 2");
+  };
+  const bool ok = H2 == 256 ? go(lz::fft_pass_kernel<lz::FFT_IN_COMPLEX, lz::FFT_OUT_HALF_SPECTRUM, 8, 256>)
+                            : go(lz::fft_pass_kernel<lz::FFT_IN_COMPLEX, lz::FFT_OUT_HALF_SPECTRUM, 7, 256>);
+  if (!ok) return false;
+  const unsigned g3 = H / 256;
+  lz::col0_unpack_kernel<256><<<g3, 256, 0, st>>>(c, col0, power, part ? part + g2.x * g2.y : nullptr);
+  *nparts = g2.x * g2.y + g3;
+  return cuda_ok(cudaGetLastError(), "fft col0 unpack");
+}
+
 lorenz_status spectra_args(const uint8_t* x, uint32_t H, uint32_t W, const double* out) {
   if (!x || !out || !fft_side(H) || !fft_side(W) || (reinterpret_cast<uintptr_t>(out) & 7)) {
     lz::set_last_error("H and W must be powers of two in [2, 4096]; x and out non-null device pointers, out 8-aligned");
@@ -139,12 +188,23 @@ lorenz_status lorenz_power_spectrum(const uint8_t* x, uint32_t H, uint32_t W, do
   lz::FftPass rows = fft_rows(H, M, W, M), cols = fft_cols(H, M, M, W);
   rows.W = cols.W = W;
   cols.scale = std::ldexp(1.0, -2 * (int)ilog2((uint32_t)N));  // 1 / N^2
-  const uint32_t tiles = (cols.nseq + cols.S - 1) / cols.S;  // >= the column pass's grid
-  unsigned nparts = 0;                                          // one flatness partial per column CTA
+  const bool four = r2c && four_step_cols(H, M);
+  uint32_t tiles = (cols.nseq + cols.S - 1) / cols.S;  // >= the column pass's grid
+  if (four) {
+    const lz::FftPass c2 = four_step_stage2(H, W, M);
+    tiles = 16 * ((c2.nseq + c2.S - 1) / c2.S) + H / 256;
+  }
+  unsigned nparts = 0;  // one flatness partial per column CTA
   bool ok = !flatness ||
             cuda_ok(lz::lib_malloc_async(reinterpret_cast<void**>(&part), tiles * sizeof(double2), st), "alloc");
+  double2* col0 = nullptr;  // the four-step's packed column U[k]
+  ok = ok && (!four || cuda_ok(lz::lib_malloc_async(reinterpret_cast<void**>(&col0), H * sizeof(double2), st), "alloc"));
   cols.part = flatness ? part : nullptr;
-  if (r2c)
+  if (four)
+    ok = ok &&
+         fft_launch<lz::FFT_IN_PAIRS, lz::FFT_OUT_R2C>(rows, x, nullptr, ws, nullptr, nullptr, nullptr, st) &&
+         four_step_spectrum(H, W, M, cols.scale, ws, col0, power, cols.part, st, &nparts);
+  else if (r2c)
     ok = ok &&
          fft_launch<lz::FFT_IN_PAIRS, lz::FFT_OUT_R2C>(rows, x, nullptr, ws, nullptr, nullptr, nullptr, st) &&
          fft_launch<lz::FFT_IN_COMPLEX, lz::FFT_OUT_HALF_SPECTRUM>(cols, nullptr, ws, ws, power, nullptr, nullptr,
@@ -160,6 +220,7 @@ lorenz_status lorenz_power_spectrum(const uint8_t* x, uint32_t H, uint32_t W, do
   }
   cudaFreeAsync(ws, st);
   if (part) cudaFreeAsync(part, st);
+  if (col0) cudaFreeAsync(col0, st);
   return ok ? LORENZ_OK : LORENZ_E_CUDA;
 }
 
@@ -170,7 +231,7 @@ lorenz_status lorenz_autocorrelation(const uint8_t* x, uint32_t H, uint32_t W, d
   cudaStream_t st = (cudaStream_t)stream;
   const uint64_t N = (uint64_t)H * W;
   double2* ws = nullptr;
-  unsigned long long* aux = nullptr;  // [0] = byte sum, [1] = lag-0 value (double bits)
+  unsigned long long* aux = nullptr;  // [0] = byte sum, [1] = lag-0 value (double bits), [2] = sum of squares
   // real input (W >= 4): R2C rows of centred byte pairs -> one fused column pass (transform, |.|^2,
   // transform: FFT_OUT_POWER_FFT) over the W/2 packed columns -> C2R rows -> normalisation.
   // Three transform passes over a half-size workspace instead of four full ones; W = 2 keeps the
@@ -179,13 +240,13 @@ lorenz_status lorenz_autocorrelation(const uint8_t* x, uint32_t H, uint32_t W, d
   const uint32_t M = r2c ? W / 2 : W;
   const uint64_t Pw = r2c ? M : fft_ws_pitch(W), NW = (uint64_t)H * Pw;
   if (!cuda_ok(lz::lib_malloc_async(reinterpret_cast<void**>(&ws), NW * sizeof(double2), st), "alloc fft") ||
-      !cuda_ok(lz::lib_malloc_async(reinterpret_cast<void**>(&aux), 16, st), "alloc aux")) {
+      !cuda_ok(lz::lib_malloc_async(reinterpret_cast<void**>(&aux), 32, st), "alloc aux")) {
     if (ws) cudaFreeAsync(ws, st);
     return LORENZ_E_CUDA;
   }
   double* lag0 = reinterpret_cast<double*>(aux + 1);
   const unsigned sgrid = (unsigned)std::min<uint64_t>(4ull * sm_count(), (N + lz::kFftCta - 1) / lz::kFftCta);
-  bool ok = cuda_ok(cudaMemsetAsync(aux, 0, 16, st), "memset");
+  bool ok = cuda_ok(cudaMemsetAsync(aux, 0, 32, st), "memset");
   if (ok) {
     lz::byte_sum_kernel<<<sgrid, lz::kFftCta, 0, st>>>(x, N, aux);
     ok = cuda_ok(cudaGetLastError(), "byte sum");
@@ -197,7 +258,7 @@ lorenz_status lorenz_autocorrelation(const uint8_t* x, uint32_t H, uint32_t W, d
     cols.packed0 = 1;
     ok = fft_launch<lz::FFT_IN_PAIRS_CENTRED, lz::FFT_OUT_R2C>(rows1, x, nullptr, ws, nullptr, aux, nullptr, st) &&
          fft_launch<lz::FFT_IN_COMPLEX, lz::FFT_OUT_POWER_FFT>(cols, nullptr, ws, ws, nullptr, nullptr, nullptr, st) &&
-         fft_launch<lz::FFT_IN_C2R, lz::FFT_OUT_REAL_PAIRS>(rows2, nullptr, ws, nullptr, r, nullptr, lag0, st);
+         fft_launch<lz::FFT_IN_C2R, lz::FFT_OUT_REAL_PAIRS>(rows2, nullptr, ws, nullptr, r, aux, nullptr, st);
   } else if (ok) {
     const lz::FftPass rows1 = fft_rows(H, W, W, Pw), cols1 = fft_cols(H, W, Pw, Pw);
     const lz::FftPass rows2 = fft_rows(H, W, Pw, Pw), cols2 = fft_cols(H, W, Pw, W);
@@ -206,7 +267,7 @@ lorenz_status lorenz_autocorrelation(const uint8_t* x, uint32_t H, uint32_t W, d
          fft_launch<lz::FFT_IN_COMPLEX, lz::FFT_OUT_COMPLEX>(rows2, nullptr, ws, ws, nullptr, nullptr, nullptr, st) &&
          fft_launch<lz::FFT_IN_COMPLEX, lz::FFT_OUT_REAL>(cols2, nullptr, ws, nullptr, r, nullptr, lag0, st);
   }
-  if (ok) {
+  if (ok && !r2c) {  // the real-input pipeline normalises in its last pass (FFT_OUT_REAL_PAIRS)
     lz::autocorr_normalise_kernel<<<sgrid, lz::kFftCta, 0, st>>>(r, N, lag0);
     ok = cuda_ok(cudaGetLastError(), "normalise");
   }

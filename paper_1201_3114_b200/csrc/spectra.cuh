@@ -38,11 +38,11 @@ enum FftIn : int {
 //   mirror (-k, W-l) (real input: P(k,l) = P(-k,-l)); column 0 unpacks the DC and Nyquist columns.
 // FFT_OUT_POWER_FFT: column pass fusing transform -> |.|^2 (packed DC / Nyquist column unpacked) ->
 //   transform again (the autocorrelation's two column transforms in one HBM round trip).
-// FFT_OUT_REAL_PAIRS: the C2R row output R[m] -> real samples (2m, 2m+1) = (Re R, -Im R).
+// FFT_OUT_REAL_PAIRS: the C2R row output R[m] -> real samples (2m, 2m+1) = (Re R, -Im R), divided by the
+//   exact lag-0 value (lag0_exact; r(0,0) = 1): the autocorrelation normalised in its last pass.
 enum FftOut : int {
   FFT_OUT_COMPLEX = 0, FFT_OUT_POWER = 1, FFT_OUT_SPECTRUM = 2, FFT_OUT_REAL = 3,
-  FFT_OUT_R2C = 4, FFT_OUT_HALF_SPECTRUM = 5, FFT_OUT_POWER_FFT = 6, FFT_OUT_REAL_PAIRS = 7,
-  FFT_OUT_SMEM = 8  // the result stays in the shared-memory tile (natural order): the cluster column pass
+  FFT_OUT_R2C = 4, FFT_OUT_HALF_SPECTRUM = 5, FFT_OUT_POWER_FFT = 6, FFT_OUT_REAL_PAIRS = 7
 };
 
 struct FftPass {
@@ -60,8 +60,12 @@ struct FftPass {
   double scale;         // FFT_OUT_SPECTRUM: 1 / (HW)^2 (a power of two: exact)
   uint32_t packed0;     // FFT_OUT_POWER_FFT: sequence 0 holds the packed DC + i Nyquist column
   double2* part;        // FFT_OUT_SPECTRUM (nullable): per-CTA (sum log P, sum P) over non-DC bins
-  uint32_t kmul, kadd;  // columns: output position pos is row pos * kmul + kadd (1, 0; the cluster
-                        // column pass's CTA r holds rows r + 4 pos)
+  uint32_t kmul, kadd;  // columns: output position pos is row pos * kmul + kadd (1, 0 for a whole column);
+                        // ysplit: kadd = blockIdx.y (stage 2 of the four-step column transform)
+  uint32_t ysplit;      // 1: the grid's y index selects a block of n rows (input offset in_y_off) and the
+                        // output rows pos * kmul + blockIdx.y
+  uint64_t in_y_off;    // input element offset per blockIdx.y
+  double2* col0_out;    // stage 2 (nullable): sequence 0's transform U[k] goes here instead of P
 };
 
 // CTA threads: 256, except 512 for 4096-point column passes (S = 2 adjacent columns per CTA,
@@ -86,6 +90,9 @@ inline FftPass fft_plan(uint32_t n, uint32_t logn, uint32_t nseq, bool rows) {
   if (k > 1) p.pitch += ((8 / k) - p.pitch % 8 + 8) % 8;  // pitch = 8/k (mod 8)
   p.kmul = 1;
   p.kadd = 0;
+  p.ysplit = 0;
+  p.in_y_off = 0;
+  p.col0_out = nullptr;
   p.npass = 0;
   uint32_t L = logn;
   while (L >= 4) { p.rlog[p.npass++] = 4; L -= 4; }
@@ -204,7 +211,19 @@ struct FftIo {
   const double2* thi;    // shared: exp(-2 pi i 64 m / n), m < n / 64
   const double2* t2lo;   // shared (R2C / C2R): exp(-2 pi i m / 2n), m < 64
   const double2* t2hi;   // shared (R2C / C2R): exp(-2 pi i 64 m / 2n), m < 2n / 64
+  double c0 = 0.0;       // FFT_OUT_REAL_PAIRS: the unnormalised lag-0 value (lag0_exact) and its reciprocal
+  double inv_c0 = 0.0;
 };
+
+// The lag-0 value of the real-input autocorrelation pipeline's unnormalised output: the second
+// forward transform scales by N and the C2R pre-processing by 1/2, so it is (N/2) c(0,0) with
+// c(0,0) = sum_ij (x_ij - mean)^2 = (N sum x^2 - (sum x)^2) / N, i.e. (N sum x^2 - (sum x)^2) / 2,
+// from the exact byte sums; the only rounding is the 128-bit integer's conversion to binary64
+// (the normaliser, fused into the last pass instead of a separate pass over r)
+__device__ __forceinline__ double lag0_exact(const unsigned long long* sums, uint64_t N) {
+  const unsigned __int128 num = (unsigned __int128)N * sums[2] - (unsigned __int128)sums[0] * sums[0];
+  return __dmul_rn((double)num, 0.5);
+}
 
 template <int N>
 __device__ __forceinline__ double2 twid2(const FftIo& io, uint32_t m) {  // exp(-2 pi i m / 2N)
@@ -239,7 +258,7 @@ __device__ __forceinline__ double2 fft_load(const FftPass& p, const FftIo& io, u
     return make_double2(__dadd_rn(ge.x, go.y), __dsub_rn(ge.y, go.x));  // ge - i go
   }
   const uint64_t g = p.rows ? seq * p.in_pitch + idx : (uint64_t)idx * p.in_pitch + seq;
-  if (IN == FFT_IN_COMPLEX) return io.cin[g];
+  if (IN == FFT_IN_COMPLEX) return io.cin[g + (p.ysplit ? blockIdx.y * p.in_y_off : 0)];
   const double b = io.sb ? (double)io.sb[(seq - io.seq0) * N + idx] : (double)io.bytes[g];
   return make_double2(IN == FFT_IN_CENTRED ? __dsub_rn(b, io.mean) : b, 0.0);  // exact (HW = 2^k)
 }
@@ -247,7 +266,8 @@ __device__ __forceinline__ double2 fft_load(const FftPass& p, const FftIo& io, u
 template <int OUT>
 __device__ __forceinline__ void fft_store(const FftPass& p, const FftIo& io, uint64_t seq, uint32_t pos, double2 v,
                                           FlatAcc& acc) {
-  const uint64_t i = p.rows ? seq : (uint64_t)pos * p.kmul + p.kadd, j = p.rows ? pos : seq;  // (row, column)
+  const uint64_t i = p.rows ? seq : (uint64_t)pos * p.kmul + (p.ysplit ? blockIdx.y : p.kadd);  // (row, column)
+  const uint64_t j = p.rows ? pos : seq;
   if (OUT == FFT_OUT_COMPLEX) {
     io.cout[i * p.out_pitch + j] = v;
   } else if (OUT == FFT_OUT_POWER) {
@@ -257,9 +277,11 @@ __device__ __forceinline__ void fft_store(const FftPass& p, const FftIo& io, uin
     const double P = __dmul_rn(__dadd_rn(__dmul_rn(v.x, v.x), __dmul_rn(v.y, v.y)), p.scale);
     io.rout[o] = P;
     if (p.part && (i | j) != 0) acc.add(P);  // flatness over the non-DC bins
-  } else if (OUT == FFT_OUT_REAL_PAIRS) {  // rows only: samples (seq, 2 pos), (seq, 2 pos + 1)
-    reinterpret_cast<double2*>(io.rout + seq * p.W)[pos] = make_double2(v.x, -v.y);
-    if (seq == 0 && pos == 0) *io.lag0 = v.x;
+  } else if (OUT == FFT_OUT_REAL_PAIRS) {  // rows only: r at (seq, 2 pos), (seq, 2 pos + 1), normalised
+    double2 o = make_double2(0.0, 0.0);     // a zero-variance input: r = 0 off the origin
+    if (io.c0 > 0.0) o = make_double2(__dmul_rn(v.x, io.inv_c0), -__dmul_rn(v.y, io.inv_c0));
+    if (seq == 0 && pos == 0) o.x = 1.0;    // r(0,0) = 1 (Q25)
+    reinterpret_cast<double2*>(io.rout + seq * p.W)[pos] = o;
   } else if (OUT == FFT_OUT_HALF_SPECTRUM) {  // column j in [1, W/2): (k, j) and its mirror (-k, W - j)
     const double P = __dmul_rn(__dadd_rn(__dmul_rn(v.x, v.x), __dmul_rn(v.y, v.y)), p.scale);
     const uint64_t i2 = (p.H - i) & (p.H - 1), j2 = p.W - j;
@@ -324,16 +346,14 @@ __device__ __forceinline__ void fft_pass(const FftPass& p, const FftIo& io, doub
     for (int u = 0; u < R; ++u) {
       const uint32_t pos = (j - k) * R + k + u * LS;
       const double2 v = a[g * R + bitrev_c<R>(u)];
-      if (LAST && !(OUT == FFT_OUT_R2C || OUT == FFT_OUT_POWER_FFT || OUT == FFT_OUT_SMEM ||
-                    (OUT == FFT_OUT_HALF_SPECTRUM && seq == 0))) {
+      if (LAST && !(OUT == FFT_OUT_R2C || OUT == FFT_OUT_POWER_FFT || (OUT == FFT_OUT_HALF_SPECTRUM && seq == 0))) {
         if (valid) fft_store<OUT>(p, io, seq, pos, v, acc);
       } else {
         Xs[fft_pad(pos)] = v;  // exchange, or the input of a shared-memory epilogue
       }
     }
   }
-  if (!LAST || OUT == FFT_OUT_R2C || OUT == FFT_OUT_HALF_SPECTRUM || OUT == FFT_OUT_POWER_FFT || OUT == FFT_OUT_SMEM)
-    __syncthreads();
+  if (!LAST || OUT == FFT_OUT_R2C || OUT == FFT_OUT_HALF_SPECTRUM || OUT == FFT_OUT_POWER_FFT) __syncthreads();
 }
 
 // the passes of an N = 2^LOGN transform: radix 16 while >= 4 bits remain, then the remainder
@@ -365,7 +385,7 @@ __device__ __forceinline__ void flat_partial(const FlatAcc& fa, double2* part) {
     if (threadIdx.x == 0) {
       double2 t = red[0];
       for (int w = 1; w < CTA / 32; ++w) t = make_double2(__dadd_rn(t.x, red[w].x), __dadd_rn(t.y, red[w].y));
-      part[blockIdx.x] = t;
+      part[blockIdx.x + (uint64_t)gridDim.x * blockIdx.y] = t;
     }
   }
 }
@@ -467,6 +487,10 @@ __global__ void __launch_bounds__(CTA, 512 / CTA)
   FftIo io{bytes, nullptr, seq0, cin, cout, rout, lag0, 0.0, tws, tws + 64, nullptr, nullptr};
   if (IN == FFT_IN_CENTRED || IN == FFT_IN_PAIRS_CENTRED)
     io.mean = __ddiv_rn((double)*sum, (double)p.H * (double)p.W);
+  if (OUT == FFT_OUT_REAL_PAIRS) {
+    io.c0 = lag0_exact(sum, (uint64_t)p.H * p.W);
+    io.inv_c0 = io.c0 > 0.0 ? __drcp_rn(io.c0) : 0.0;
+  }
   if constexpr ((IN == FFT_IN_BYTES || IN == FFT_IN_CENTRED || IN == FFT_IN_PAIRS || IN == FFT_IN_PAIRS_CENTRED) &&
                 N >= 16 && CTA == 256) {
     constexpr int BPE = (IN == FFT_IN_PAIRS || IN == FFT_IN_PAIRS_CENTRED) ? 2 : 1;  // bytes per element
@@ -502,7 +526,13 @@ __global__ void __launch_bounds__(CTA, 512 / CTA)
   }
   if constexpr (OUT == FFT_OUT_R2C) r2c_epilogue<N>(p, io, Xs, tid, seq, valid, tw2s, tw2s + 64);
   if constexpr (OUT == FFT_OUT_HALF_SPECTRUM)
-    if (seq0 == 0 && s == 0 && active) half_col0_epilogue<N>(p, io, Xs, tid, fa);
+    if (seq0 == 0 && s == 0 && active) {
+      if (p.col0_out) {  // four-step stage 2: U[k] of the packed column, k = pos kmul + blockIdx.y
+        for (uint32_t k2 = tid; k2 < (uint32_t)N; k2 += T) p.col0_out[(uint64_t)k2 * p.kmul + blockIdx.y] = Xs[fft_pad(k2)];
+      } else {
+        half_col0_epilogue<N>(p, io, Xs, tid, fa);
+      }
+    }
   if ((OUT == FFT_OUT_SPECTRUM || OUT == FFT_OUT_HALF_SPECTRUM) && p.part) flat_partial<CTA>(fa, p.part);
 }
 
@@ -575,24 +605,99 @@ __global__ void __launch_bounds__(CTA, 512 / CTA)
 }
 
 
+// ---------------------------------------------------------------- four-step column transform
+// The power spectrum's column transforms for H = 16 H2 (H = 2048, 4096): stage 1 below, then stage 2 =
+// fft_pass_kernel<FFT_IN_COMPLEX, FFT_OUT_HALF_SPECTRUM, log2 H2> with ysplit (blockIdx.y = k1), then
+// col0_unpack_kernel. With n = H2 n1 + n2 and k = k1 + 16 k2:
+//   X[k1 + 16 k2] = sum_{n2} W_H2^{n2 k2} ( W_H^{n2 k1} sum_{n1<16} x[H2 n1 + n2] W_16^{n1 k1} ).
+// Stage 1 does the 16-point DFTs and twiddles in registers, one thread per (n2, column), a warp covering
+// 4 n2 x 8 adjacent columns (128-byte row segments), and writes y[k1] in place at row H2 k1 + n2 (it
+// reads exactly the 16 elements it writes); stage 2 runs the H2-point transforms over H2 consecutive
+// rows per k1, 16 columns per CTA, and writes P at rows k1 + 16 k2. The single-pass alternative moves
+// 32-byte row segments of 2 columns and is bound by the LSU.
+template <int LOGN>
+__global__ void __launch_bounds__(256) fft_col_stage1_kernel(const FftPass p, double2* __restrict__ ws) {
+  constexpr int N = 1 << LOGN, N2 = N / 16;
+  __shared__ double2 tw[64 + N / 64];
+  for (uint32_t i = threadIdx.x; i < 64 + N / 64; i += 256) tw[i] = twiddle_exact(i < 64 ? i : 64 * (i - 64), N);
+  __syncthreads();
+  const uint32_t c = threadIdx.x & 7, n2 = blockIdx.x * 32 + (threadIdx.x >> 3);
+  const uint64_t col = (uint64_t)blockIdx.y * 8 + c;
+  if (n2 >= (uint32_t)N2 || col >= p.nseq) return;
+  double2 a[16];
+#pragma unroll
+  for (int t = 0; t < 16; ++t) a[t] = ws[(uint64_t)(N2 * t + n2) * p.in_pitch + col];
+  dft_dif<16>(a, 0);  // y_u in a[bitrev16(u)]
+  auto tw_at = [&](uint32_t m) { return cmul(tw[m & 63], tw[64 + (m >> 6)]); };  // exp(-2 pi i m / N), m < N
+  const double2 one = make_double2(1.0, 0.0);
+  const double2 w1 = n2 ? tw_at(n2) : one, w2 = n2 ? tw_at(2 * n2) : one, w4 = n2 ? tw_at(4 * n2) : one;
+  const double2 w8 = n2 ? tw_at(8 * n2) : one, w3 = cmul(w1, w2), w12 = cmul(w4, w8);
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    double2 v = a[bitrev_c<16>(u)];
+    if (u) {
+      const int lo = u & 3, hi = u & 12;
+      const double2 wl = lo == 1 ? w1 : lo == 2 ? w2 : w3;
+      const double2 wh = hi == 4 ? w4 : hi == 8 ? w8 : w12;
+      v = cmul(v, lo == 0 ? wh : hi == 0 ? wl : cmul(wl, wh));
+    }
+    ws[(uint64_t)(N2 * u + n2) * p.in_pitch + col] = v;
+  }
+}
+
+// The packed DC / Nyquist column after stage 2 (U[k] gathered from the 16 k1 blocks): the same
+// unpacking as half_col0_epilogue; CTA b's flatness partial goes to part[b].
+template <int CTA>
+__global__ void __launch_bounds__(CTA) col0_unpack_kernel(const FftPass p, const double2* __restrict__ u,
+                                                          double* __restrict__ rout, double2* part) {
+  FlatAcc fa;
+  const uint32_t N = p.H;
+  for (uint32_t k = blockIdx.x * CTA + threadIdx.x; k < N; k += CTA * gridDim.x) {
+    const double2 a = u[k], bz = u[(N - k) & (N - 1)];
+    const double2 A = make_double2(__dmul_rn(__dadd_rn(a.x, bz.x), 0.5), __dmul_rn(__dsub_rn(a.y, bz.y), 0.5));
+    const double2 Bv = make_double2(__dmul_rn(__dadd_rn(a.y, bz.y), 0.5), __dmul_rn(__dsub_rn(bz.x, a.x), 0.5));
+    const double P0 = __dmul_rn(__dadd_rn(__dmul_rn(A.x, A.x), __dmul_rn(A.y, A.y)), p.scale);
+    const double P1 = __dmul_rn(__dadd_rn(__dmul_rn(Bv.x, Bv.x), __dmul_rn(Bv.y, Bv.y)), p.scale);
+    const uint64_t row = ((k + p.H / 2) & (p.H - 1)) * p.W;
+    rout[row + p.W / 2] = P0;  // column 0 -> centred column W/2
+    rout[row] = P1;            // column W/2 -> centred column 0
+    if (part) {
+      if (k != 0) fa.add(P0);
+      fa.add(P1);
+    }
+  }
+  if (part) flat_partial<CTA>(fa, part);
+}
+
 constexpr int kFftCta = 256;  // the reductions below
 
-// sum of the H*W bytes (the mean of the autocorrelation's centring; < 2^36, exact)
+// sum of the H*W bytes (the mean of the autocorrelation's centring; < 2^36, exact) in out[0] and
+// the sum of their squares (< 2^44, exact) in out[2]
 __global__ void __launch_bounds__(kFftCta) byte_sum_kernel(const uint8_t* __restrict__ x, uint64_t n,
                                                            unsigned long long* __restrict__ out) {
-  unsigned long long acc = 0;
+  unsigned long long acc = 0, acc2 = 0;
   const uint64_t t0 = (uint64_t)blockIdx.x * kFftCta + threadIdx.x, step = (uint64_t)gridDim.x * kFftCta;
-  if ((reinterpret_cast<uintptr_t>(x) & 15) == 0 && n % 16 == 0) {  // 16 bytes per load, SAD-summed
+  if ((reinterpret_cast<uintptr_t>(x) & 15) == 0 && n % 16 == 0) {  // 16 bytes per load, SAD / dp4a sums
     for (uint64_t i = t0; i < n / 16; i += step) {
       const uint4 v = __ldcs(reinterpret_cast<const uint4*>(x) + i);
       acc += __vsadu4(v.x, 0u) + __vsadu4(v.y, 0u) + __vsadu4(v.z, 0u) + __vsadu4(v.w, 0u);
+      acc2 += __dp4a(v.x, v.x, 0u) + __dp4a(v.y, v.y, 0u) + __dp4a(v.z, v.z, 0u) + __dp4a(v.w, v.w, 0u);
     }
   } else {
-    for (uint64_t i = t0; i < n; i += step) acc += x[i];
+    for (uint64_t i = t0; i < n; i += step) {
+      acc += x[i];
+      acc2 += (unsigned)x[i] * x[i];
+    }
   }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, acc);
+  for (int o = 16; o > 0; o >>= 1) {
+    acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    acc2 += __shfl_xor_sync(0xffffffffu, acc2, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (acc) atomicAdd(out, acc);
+    if (acc2) atomicAdd(out + 2, acc2);
+  }
 }
 
 // r = c / c(0,0); a zero-variance input (c(0,0) = 0 exactly) gives the S:436 convention (Q25)
