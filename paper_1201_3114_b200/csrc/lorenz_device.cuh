@@ -320,13 +320,25 @@ __device__ __forceinline__ void euler_step(double& x, double& y, double& z, doub
 #ifndef LZ_PIN_MASK
 #define LZ_PIN_MASK 3
 #endif
+#ifndef LZ_IMM_CONST
+#define LZ_IMM_CONST 0
+#endif
 template <int INTEG, bool PIN = false>
 __device__ __forceinline__ void integrate(double& x, double& y, double& z, const DevConst& C) {
+#if LZ_IMM_CONST
+  // sigma = 10, rho = 28 and beta = RN(8/3) are fixed by the cipher (the key holds the same bit
+  // patterns): compile-time operands, so the FP64 instructions read them as immediates / constant-bank
+  // operands instead of general registers
+  constexpr double S = 10.0, R = 28.0, Bt = 2.6666666666666665;
+  double h = C.h, h2 = C.h2, h6 = C.h6;
+  if (PIN && ((LZ_PIN_MASK >> INTEG) & 1)) {
+#else
   double S = C.sigma, R = C.rho, Bt = C.beta, h = C.h, h2 = C.h2, h6 = C.h6;
   if (PIN && ((LZ_PIN_MASK >> INTEG) & 1)) {
     asm volatile("add.rn.f64 %0, %0, 0d0000000000000000;" : "+d"(S));
     asm volatile("add.rn.f64 %0, %0, 0d0000000000000000;" : "+d"(R));
     asm volatile("add.rn.f64 %0, %0, 0d0000000000000000;" : "+d"(Bt));
+#endif
     asm volatile("add.rn.f64 %0, %0, 0d0000000000000000;" : "+d"(h));
     asm volatile("add.rn.f64 %0, %0, 0d0000000000000000;" : "+d"(h2));
     asm volatile("add.rn.f64 %0, %0, 0d0000000000000000;" : "+d"(h6));
@@ -756,6 +768,9 @@ __device__ __forceinline__ void seg_slot_range(const SegPlan& P, uint64_t k, uin
   x1 = x0 + P.cq + (uint64_t)((P.wpc - 1 - r) >> 2) * P.dq;
 }
 constexpr int kSegWords = 18;  // u64 words of one lane's handed-over state
+#ifndef LZ_SEG_UNIFIED
+#define LZ_SEG_UNIFIED 0
+#endif
 
 __device__ __forceinline__ void seg_save(uint64_t* dst, uint32_t lane, const Chain& c, const LaneAcc& a) {
   const uint64_t w[kSegWords] = {
@@ -853,6 +868,43 @@ __global__ void __launch_bounds__(CTA, 1)
   }
 #endif
 
+#if LZ_SEG_UNIFIED
+  // One loop over the slot's pieces with a single inlined copy of the character loop (so ptxas can
+  // keep the integrator's constants in uniform registers): piece 0 may be the FIRST chunks [0, a) of
+  // the unit cut at X0 (hands its state to slot k-1), then whole units, then possibly the LAST chunks
+  // [a', Q) of the unit cut at X1 (takes its state from slot k+1).
+  const uint64_t u_end = (X1 + Q - 1) / Q;  // one past the last unit the slot touches
+  for (; u < u_end; ++u) {
+    const bool first_piece = u * Q < X0;                       // starts before X0: chunks [0, (u+1)Q - X0)
+    const bool last_piece = !first_piece && (u + 1) * Q > X1;  // ends after X1: chunks [(u+1)Q - X1, Q)
+    const uint64_t c0 = last_piece ? (u + 1) * Q - X1 : 0;
+    const uint64_t c1 = first_piece ? (u + 1) * Q - X0 : Q;
+    const LaneIO io = lane_io<OP>(C, in, out, u * 32 + lane);
+    Chain ch;
+    LaneAcc acc{0, 0, true, false};
+    if (last_piece) {
+      SEG_TRACE(k, 2, gtimer());
+      if (lane == 0)
+        while (ld_acquire_u32(seg_flag + k + 1) == 0) __nanosleep(256);
+      __syncwarp();
+      SEG_TRACE(k, 3, gtimer());
+      (void)ld_acquire_u32(seg_flag + k + 1);
+      seg_load(seg_state + (k + 1) * (kSegWords * 32), lane, ch, acc);
+    } else if (io.active) {
+      key_schedule(C.batch ? Kb[io.s] : K1, C.fast != 0, (uint32_t)io.bl, C.variant, ch);
+    }
+    run_chars<OP, INTEG, WIN, true>(C, io, ch, acc, wst, theta_tab, 16 * c0, 16 * c1, lane);
+    if (first_piece) {
+      seg_save(seg_state + k * (kSegWords * 32), lane, ch, acc);
+      __threadfence();
+      __syncwarp();
+      if (lane == 0) st_release_u32(seg_flag + k, 1u);
+      SEG_TRACE(k, 1, gtimer());
+    } else {
+      finish_lanes<OP>(C, io, acc, res, tags_batch, block_ok, lane);
+    }
+  }
+#else
   if (X0 % Q) {  // first piece: chunks [0, a) of unit u, which slot k-1 finishes
     const uint64_t a = (u + 1) * Q - X0;
     const LaneIO io = lane_io<OP>(C, in, out, u * 32 + lane);
@@ -890,6 +942,7 @@ __global__ void __launch_bounds__(CTA, 1)
     run_chars<OP, INTEG, WIN, true>(C, io, ch, acc, wst, theta_tab, 16 * a, 16 * Q, lane);
     finish_lanes<OP>(C, io, acc, res, tags_batch, block_ok, lane);
   }
+#endif
   SEG_TRACE(k, 4, gtimer());
 }
 
