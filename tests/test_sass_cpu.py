@@ -8,8 +8,8 @@ DESIGN.md §2 in RN with no contraction into FMA:
   Euler (NEXT-1):    28 DADD + 32 DMUL per 4-step unrolled iteration, 7 + 8 for the remainder;
   RK4-FMA (NEXT-3):  7 DADD + 8 DMUL + 30 DFMA per step (the FMA sites of DESIGN.md §2b).
 
-and nothing else inside a loop but its counter / branch (and, for the FMA form in the balanced
-kernel, the constants' uniform-register reloads).
+and nothing else inside a loop but its counter / branch and the handling of its constants
+(uniform-register moves / reloads).
 
 Checked for every innermost FP64 loop of every chain-kernel instantiation (wave kernel: its
 loop copies; balanced kernel: the first-piece, whole-unit and last-piece copies), plus no local
@@ -34,16 +34,16 @@ pytestmark = pytest.mark.skipif(shutil.which("cuobjdump") is None and not os.pat
     "/usr/local/cuda/bin/cuobjdump"), reason="cuobjdump not installed")
 
 RK4, EULER, RK4_FMA = 0, 1, 2
-# FP64 mix of each integration loop shape, and the non-FP64 instructions it may carry: 3 = counter,
-# compare, branch; 4 = the unrolled Euler loop's extra counter step; 6 = the balanced kernel's FMA
-# loop, which reloads the six constants into uniform registers every step (3 LDCU.128, off the FP64
-# pipe; DESIGN.md §4 "constants in registers")
+# FP64 mix of each integration loop shape. Besides it a loop may only carry its counter, compare and
+# branch and the handling of its constants — UMOV (beta into a uniform register, RK4 / Euler take
+# sigma, rho, beta as compile-time operands) and LDCU (the balanced kernel's FMA loop reloads its six
+# constants into uniform registers every step, off the FP64 pipe) — at most 6 of them.
 EXPECTED = {
     RK4: [{"DADD": 43, "DMUL": 32, "DFMA": 0}],
     EULER: [{"DADD": 28, "DMUL": 32, "DFMA": 0}, {"DADD": 7, "DMUL": 8, "DFMA": 0}],
     RK4_FMA: [{"DADD": 7, "DMUL": 8, "DFMA": 30}],
 }
-OTHER = {RK4: {3}, EULER: {3, 4}, RK4_FMA: {3, 6}}
+ALLOWED_OTHER = {"IADD3", "VIADD", "UIADD3", "IMAD", "MOV", "ISETP", "UISETP", "BRA", "UMOV", "LDCU"}
 
 
 def fp64(lp):
@@ -70,7 +70,8 @@ def test_integration_loops_exact_op_mix(loops):
         want = EXPECTED[integ]
         assert found, (kern, op, integ, cta, "no integration loop found")
         for lp in found:
-            assert fp64(lp) in want and lp["other"] in OTHER[integ], (kern, op, integ, cta, lp)
+            assert fp64(lp) in want, (kern, op, integ, cta, lp)
+            assert lp["other"] <= 6 and set(lp["other_ops"]) <= ALLOWED_OTHER, (kern, op, integ, cta, lp)
         # every expected loop shape is present, in every inlined copy of the character loop
         copies = 3 if kern == "lorenz_chain_seg_kernel" else 1
         for w in want:
@@ -116,4 +117,4 @@ def test_negative_control_contraction(tmp_path, fmad, contracted):
         assert all(lp["DFMA"] > 0 for lp in found), found
         assert all(fp64(lp) not in EXPECTED[RK4] for lp in found)
     else:
-        assert all(fp64(lp) in EXPECTED[RK4] and lp["other"] == 3 for lp in found), found
+        assert all(fp64(lp) in EXPECTED[RK4] and lp["other"] == 3 for lp in found), found  # counter, compare, branch

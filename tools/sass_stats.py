@@ -78,7 +78,8 @@ def innermost_fp64_loops(ins, min_fp64=10):
         c = collections.Counter(o.split(".")[0] for ad, o, _ in ins if t <= ad <= a)
         if c["DADD"] + c["DMUL"] + c["DFMA"] >= min_fp64 and not c["MUFU"]:
             out.append({"DADD": c["DADD"], "DMUL": c["DMUL"], "DFMA": c["DFMA"],
-                        "other": sum(c.values()) - c["DADD"] - c["DMUL"] - c["DFMA"]})
+                        "other": sum(c.values()) - c["DADD"] - c["DMUL"] - c["DFMA"],
+                        "other_ops": sorted({o for o in c if o not in ("DADD", "DMUL", "DFMA")})})
     return out
 
 
