@@ -54,3 +54,18 @@ def test_two_ranks_one_gpu_gloo(workload):
     else:
         s = d2["c5_stats_rank0"]
         assert s["untouched_blocks_identical"] and s["ct_entropy_min"] > 7.9
+
+
+def test_torchrun_one_rank_nccl():
+    """The driver's scaling runs launch bench.py under torchrun with NCCL: at N = 1 the same flow runs
+    here for real (NCCL communicator, all_gather_object of the per-rank record, 16-byte tag all-gather,
+    MIN verdict), and the line reports the communicator's world size and backend."""
+    args = ["bench.py", "--workload", "c3", "--steps", "2", "--warmup", "3", "--no-cpu-baseline", "--gpus", "1"]
+    lines = run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1",
+                 "--master-addr", "127.0.0.1", "--master-port", "29534"] + args, os.environ.copy())
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    rk = d["ranks"]
+    assert rk["world_size"] == 1 and rk["backend"] == "nccl" and len(rk["per_rank"]) == 1
+    assert d["validated"]["round_trip"] is True and d["validated"]["tag_matches_oracle"] is True
+    assert rk["per_rank"][0]["tag"] == d["validated"]["tag_xor"]
