@@ -336,6 +336,7 @@ constexpr uint64_t kPoolKeep = 256ull << 20;
 cudaError_t lib_malloc_async(void** p, size_t bytes, cudaStream_t st) {
   static std::mutex mu;
   static cudaMemPool_t pools[64] = {};
+  static bool tried[64] = {};
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
@@ -343,19 +344,24 @@ cudaError_t lib_malloc_async(void** p, size_t bytes, cudaStream_t st) {
   cudaMemPool_t pool;
   {
     std::lock_guard<std::mutex> lk(mu);
-    if (!pools[dev]) {
+    if (!tried[dev]) {
+      tried[dev] = true;
       cudaMemPoolProps props;
       std::memset(&props, 0, sizeof props);
       props.allocType = cudaMemAllocationTypePinned;
       props.location.type = cudaMemLocationTypeDevice;
       props.location.id = dev;
-      if ((e = cudaMemPoolCreate(&pools[dev], &props)) != cudaSuccess) return e;
-      uint64_t keep = kPoolKeep;
-      cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &keep);
+      if (cudaMemPoolCreate(&pools[dev], &props) == cudaSuccess) {
+        uint64_t keep = kPoolKeep;
+        cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &keep);
+      } else {  // no pool of our own (e.g. a device without stream-ordered pools): the default one
+        cudaGetLastError();
+        pools[dev] = nullptr;
+      }
     }
     pool = pools[dev];
   }
-  return cudaMallocFromPoolAsync(p, bytes, pool, st);
+  return pool ? cudaMallocFromPoolAsync(p, bytes, pool, st) : cudaMallocAsync(p, bytes, st);
 }
 }  // namespace lz
 
