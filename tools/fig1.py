@@ -38,10 +38,12 @@ def main():
     torch.cuda.synchronize()
     sec = e0.elapsed_time(e1) / 1e3
     ops = a.lanes * (a.skip + a.samples * a.stride) * 75
+    digit_ops = a.lanes * a.samples * 9  # |v| 10^2, 10^4, 10^6 for 3 coordinates per sample (DMUL)
     h = hist.cpu().numpy().reshape(3, 4, 128)
     out = {"what": "Fig.1 digit histograms (NEXT-4)", "lanes": a.lanes, "skip": a.skip, "samples": a.samples,
            "stride": a.stride, "seconds": round(sec, 4),
-           "fp64_pipe_frac": round(ops / sec / (148 * 64 * 1965e6), 4), "coords": {}}
+           "fp64_pipe_frac": round(ops / sec / (148 * 64 * 1965e6), 4),
+           "fp64_pipe_frac_incl_digit_products": round((ops + digit_ops) / sec / (148 * 64 * 1965e6), 4), "coords": {}}
     for c, name in enumerate("xyz"):
         nz = np.nonzero(h[c, 0])[0] - 64
         chis = []
