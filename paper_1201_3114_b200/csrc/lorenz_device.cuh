@@ -546,10 +546,49 @@ struct LaneAcc {
   bool guard_ok, bad;
 };
 
+// Stage-in of one window: chunk c of row `row` (16 bytes at w0 + 16 c), zero past the lane's
+// characters and (SEG) past the window limit wlim; the sentinel bytes are synthesised on encrypt.
+template <int OP, int WIN, bool SEG>
+__device__ __forceinline__ void stage_load(const LaneIO& io, uint64_t w0, uint64_t wlim, uint32_t lane,
+                                           uint4 (&v)[WIN / 16]) {
+  constexpr int CHUNKS = WIN / 16;
+#pragma unroll
+  for (int it = 0; it < CHUNKS; ++it) {
+    const uint32_t q = it * 32 + lane, row = q / CHUNKS, c = q % CHUNKS;
+    const uint8_t* r_in = (const uint8_t*)__shfl_sync(0xffffffffu, (unsigned long long)io.irow, row);
+    const uint64_t r_len = __shfl_sync(0xffffffffu, io.len, row);
+    const uint64_t r_tot = __shfl_sync(0xffffffffu, io.total, row);
+    const uint64_t pos = w0 + 16 * c;
+    v[it] = make_uint4(0, 0, 0, 0);
+    if (pos < r_tot && (!SEG || pos < wlim)) {
+      const uint64_t r_src = (OP == OP_ENC) ? r_len : r_tot;  // bytes readable from memory
+      if (pos + 16 <= r_src) {
+        v[it] = ld_stream(r_in + pos);
+      } else if (OP == OP_ENC && pos >= r_len && ((r_len & 15) == 0)) {
+        v[it] = make_uint4((uint32_t)kSentLo, (uint32_t)(kSentLo >> 32), (uint32_t)kSentHi,
+                           (uint32_t)(kSentHi >> 32));
+      } else {
+        uint32_t wv[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const uint64_t j = pos + i;
+          uint32_t bv = 0;
+          if (j < r_src) bv = r_in[j];
+          else if (OP == OP_ENC && j < r_tot) bv = sent_byte((uint32_t)(j - r_len));
+          wv[i >> 2] |= bv << (8 * (i & 3));
+        }
+        v[it] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+      }
+    }
+  }
+}
+
 // Characters [c0, c1) of every lane of the warp: stage in, run the chain, stage out, one
 // WIN-character window at a time. c0 is a multiple of 16; c1 is a multiple of 16 (SEG: the
 // balanced kernel, which also keeps its constants in registers, see integrate) or at least
 // every lane's total (the wave kernel). Lanes stop at their own total. Warp-uniform control flow.
+// (Issuing the next window's loads before this window's characters — a register prefetch — measured
+// no faster, even with the buffers in mapped host memory: other warps cover the wait.)
 template <int OP, int INTEG, int WIN, bool SEG = false>
 __device__ __forceinline__ void run_chars(const DevConst& C, const LaneIO& io, Chain& ch, LaneAcc& acc,
                                           uint8_t* wst, const double* theta_tab, uint64_t c0, uint64_t c1,
@@ -561,35 +600,12 @@ __device__ __forceinline__ void run_chars(const DevConst& C, const LaneIO& io, C
     // (and leaving the checks out keeps its register allocation: RK4-FMA 92.8 % -> 95.0 %)
     const uint64_t wlim = (!SEG || w0 + WIN < c1) ? w0 + WIN : c1;
     // ---- stage in: 32 rows x WIN bytes, coalesced 16-B chunks ----
+    uint4 v[CHUNKS];
+    stage_load<OP, WIN, SEG>(io, w0, wlim, lane, v);
 #pragma unroll
     for (int it = 0; it < CHUNKS; ++it) {
       const uint32_t q = it * 32 + lane, row = q / CHUNKS, c = q % CHUNKS;
-      const uint8_t* r_in = (const uint8_t*)__shfl_sync(0xffffffffu, (unsigned long long)io.irow, row);
-      const uint64_t r_len = __shfl_sync(0xffffffffu, io.len, row);
-      const uint64_t r_tot = __shfl_sync(0xffffffffu, io.total, row);
-      const uint64_t pos = w0 + 16 * c;
-      uint4 v = make_uint4(0, 0, 0, 0);
-      if (pos < r_tot && (!SEG || pos < wlim)) {
-        const uint64_t r_src = (OP == OP_ENC) ? r_len : r_tot;  // bytes readable from memory
-        if (pos + 16 <= r_src) {
-          v = ld_stream(r_in + pos);
-        } else if (OP == OP_ENC && pos >= r_len && ((r_len & 15) == 0)) {
-          v = make_uint4((uint32_t)kSentLo, (uint32_t)(kSentLo >> 32), (uint32_t)kSentHi,
-                         (uint32_t)(kSentHi >> 32));
-        } else {
-          uint32_t wv[4] = {0, 0, 0, 0};
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const uint64_t j = pos + i;
-            uint32_t bv = 0;
-            if (j < r_src) bv = r_in[j];
-            else if (OP == OP_ENC && j < r_tot) bv = sent_byte((uint32_t)(j - r_len));
-            wv[i >> 2] |= bv << (8 * (i & 3));
-          }
-          v = make_uint4(wv[0], wv[1], wv[2], wv[3]);
-        }
-      }
-      *reinterpret_cast<uint4*>(wst + row * ROW + 16 * c) = v;
+      *reinterpret_cast<uint4*>(wst + row * ROW + 16 * c) = v[it];
     }
     __syncwarp();
 
