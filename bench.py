@@ -543,7 +543,7 @@ def main():
             traffic = json.load(open(tpath)).get("dram_bytes_per_launch_c4_rank_of", {}).get(str(world))
         except (ValueError, OSError):
             traffic = None
-    c3path = os.path.join(ROOT, "profiles", "ncu_seg_kernel_c3_r01.json")
+    c3path = os.path.join(ROOT, "profiles", "ncu_seg_kernel_c3_r02.json")
     if os.path.exists(c3path) and a.workload == "c3" and a.integrator == "rk4" and a.n_it == 100 and world == 1:
         try:  # the balanced kernel's --set full capture at C3 (end-of-kernel L2 residency: writes < 65 MiB)
             traffic = json.load(open(c3path)).get("dram_bytes_per_launch")
