@@ -304,6 +304,26 @@ lorenz_status check_range(const KeyImpl* K, uint64_t n, uint64_t b0, uint64_t b1
   return LORENZ_OK;
 }
 
+// Buffers the kernels dereference must be device-accessible: device or managed memory, or page-locked
+// host memory mapped into the device's address space. Pageable host memory passed where a device
+// pointer belongs would fault inside the kernel and kill the context: refuse it (LORENZ_E_ARG) instead.
+bool device_accessible(const void* p, uint64_t len) {
+  if (!len) return true;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  if (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) return true;
+  return a.type == cudaMemoryTypeHost && a.devicePointer != nullptr;
+}
+
+lorenz_status check_device(const void* a, uint64_t na, const void* b, uint64_t nb) {
+  if (device_accessible(a, na) && device_accessible(b, nb)) return LORENZ_OK;
+  g_err = "buffer not device-accessible (pageable host memory? use the _host calls)";
+  return LORENZ_E_ARG;
+}
+
 lorenz_status finish_sync(lorenz_result* d_res, cudaStream_t st, lorenz_result* h_res) {
   if (!cuda_ok(cudaMemcpyAsync(h_res, d_res, sizeof *h_res, cudaMemcpyDeviceToHost, st), "readback"))
     return LORENZ_E_CUDA;
@@ -522,6 +542,7 @@ lorenz_status lorenz_encrypt_async(const lorenz_key* k, uint64_t n, uint64_t b0,
   if (b0 < b1) slice_bytes(K, n, b0, b1, &ptb, &ctb);
   lorenz_status s = check_range(K, n, b0, b1, pt, ptb, ct, ctb);
   if (s != LORENZ_OK || b0 == b1) return s;
+  if ((s = check_device(pt, ptb, ct, ctb)) != LORENZ_OK) return s;
   const lz::DevConst C = make_const(K, n, b0, b1 - b0);
   const lz::DevKey D = make_devkey(K);
   return cuda_ok(launch_chain<lz::OP_ENC>(C, D, nullptr, K->prm.integrator, pt, ct, res, nullptr, nullptr,
@@ -539,6 +560,7 @@ lorenz_status lorenz_decrypt_async(const lorenz_key* k, uint64_t n, uint64_t b0,
   if (b0 < b1) slice_bytes(K, n, b0, b1, &ptb, &ctb);
   lorenz_status s = check_range(K, n, b0, b1, ct, ctb, pt, ptb);
   if (s != LORENZ_OK || b0 == b1) return s;
+  if ((s = check_device(ct, ctb, pt, ptb)) != LORENZ_OK) return s;
   const lz::DevConst C = make_const(K, n, b0, b1 - b0);
   const lz::DevKey D = make_devkey(K);
   cudaStream_t st = (cudaStream_t)stream;
@@ -561,6 +583,7 @@ lorenz_status lorenz_verify_async(const lorenz_key* k, uint64_t n, uint64_t b0, 
   if (b0 < b1) slice_bytes(K, n, b0, b1, &ptb, &ctb);
   lorenz_status s = check_range(K, n, b0, b1, ct, ctb, nullptr, 0);
   if (s != LORENZ_OK || b0 == b1) return s;
+  if ((s = check_device(ct, ctb, nullptr, 0)) != LORENZ_OK) return s;
   const lz::DevConst C = make_const(K, n, b0, b1 - b0);
   const lz::DevKey D = make_devkey(K);
   return cuda_ok(launch_chain<lz::OP_VERIFY>(C, D, nullptr, K->prm.integrator, ct, nullptr, res, nullptr,
@@ -645,6 +668,8 @@ lorenz_status lorenz_encrypt_batch(const lorenz_key* keys, uint32_t S, uint64_t 
   if ((n && (!pts || !aligned16(pts) || n % 16)) || !cts || !aligned16(cts) || !tags || !aligned16(tags))
     return LORENZ_E_ARG;
   if (overlap(pts, n * S, cts, ctl * S)) return LORENZ_E_ARG;
+  if (check_device(pts, n * S, cts, ctl * S) != LORENZ_OK || check_device(tags, 16ull * S, nullptr, 0) != LORENZ_OK)
+    return LORENZ_E_ARG;
   cudaStream_t st = (cudaStream_t)stream;
   lz::DevKey* d_keys = nullptr;
   std::vector<lz::DevKey> h_keys(S);  // pageable: the H2D below is staged before it returns

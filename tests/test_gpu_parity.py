@@ -432,3 +432,29 @@ def test_host_direct_streaming(blocks):
     bad[(nb // 3) * 1040 + 5] ^= 0x10
     st, fb = L.lorenz_decrypt_host(key, n, 0, nb, bad, back_h)
     assert st == L.E_INTEGRITY and fb == nb // 3 and not back_h.any()
+
+
+def test_device_calls_refuse_pageable_host_memory():
+    """A pageable host buffer passed where a device pointer belongs is refused with E_ARG before any
+    launch (it would fault inside the kernel and kill the context); mapped pinned host memory is
+    device-accessible and works (the kernel reads it over PCIe), equal to the device result."""
+    pw = inputs.password()
+    n = 40 * 1024 + 48
+    msg = inputs.message(n)
+    key = L.lorenz_keysetup(pw, mode=L.FAST, n_it=3)
+    nb = key.num_blocks(n)
+    pageable = np.zeros(key.ct_len(n) + 64, dtype=np.uint8)
+    pg = pageable.ctypes.data + (-pageable.ctypes.data % 16)  # 16-byte aligned, still pageable
+    ct_d = torch.empty(key.ct_len(n), dtype=torch.uint8, device=DEV)
+    pt_d = torch.from_numpy(msg).to(DEV)
+    with pytest.raises(L.LorenzError) as e:
+        L.lorenz_encrypt(key, n, 0, nb, pt_d, pg)
+    assert e.value.status == L.E_ARG
+    with pytest.raises(L.LorenzError) as e:
+        L.lorenz_verify(key, n, 0, nb, pg)
+    assert e.value.status == L.E_ARG
+    tag = L.lorenz_encrypt(key, n, 0, nb, pt_d, ct_d)  # the context survived
+    pt_pin = torch.from_numpy(msg).pin_memory()
+    ct_pin = torch.zeros(key.ct_len(n), dtype=torch.uint8).pin_memory()
+    assert L.lorenz_encrypt(key, n, 0, nb, pt_pin, ct_pin) == tag
+    assert torch.equal(ct_pin, ct_d.cpu())
