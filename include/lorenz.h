@@ -26,7 +26,9 @@
  *   - Device pointers are plain CUDA device addresses (e.g. torch.Tensor.data_ptr()),
  *     16-byte aligned; the caller owns every buffer. Any device-accessible address works,
  *     including mapped page-locked host memory (UVA): the chain kernels then read and write
- *     it over PCIe themselves, window by window (the direct mode of lorenz_encrypt_host). `cuda_stream` is a cudaStream_t
+ *     it over PCIe themselves, window by window (the direct mode of lorenz_encrypt_host).
+ *     Pageable host memory is refused (LORENZ_E_ARG) by the chain and batch calls rather than
+ *     left to fault inside a kernel. `cuda_stream` is a cudaStream_t
  *     (NULL = legacy default stream). Calls without the _async suffix enqueue their
  *     work on that stream and synchronise it before returning.
  *   - Errors are returned, never raised: no abort/exit. Argument errors are reported
