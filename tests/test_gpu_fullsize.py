@@ -119,6 +119,19 @@ def test_c4_full_message_and_rank_slices():
             assert np.array_equal(got, wv[b0:b1]), (world, r, first_diff(got.ravel(), wv[b0:b1].ravel()))
         comb = bytes(np.bitwise_xor.reduce(np.frombuffer(b"".join(tags), dtype=np.uint8).reshape(world, 16)))
         assert comb == want_tag, world
+    # tamper at full size in the bench's launch: the lowest failing block is reported, the plaintext
+    # is zero-filled, verify agrees; blocks at both ends of slots and in the middle of units
+    ct_o = torch.from_numpy(want).to(DEV)
+    rng = random.Random(44)
+    for flips in ([nb - 1], [rng.randrange(nb) for _ in range(3)], [0, nb // 2]):
+        bad = ct_o.clone()
+        for b in flips:
+            bad[b * (B + 16) + rng.randrange(B + 16)] ^= 1 << rng.randrange(8)
+        back = torch.ones(n, dtype=torch.uint8, device=DEV)
+        st, fb = L.lorenz_decrypt(key, n, 0, nb, bad, back)
+        assert st == L.E_INTEGRITY and fb == min(flips) and not back.any(), (flips, st, fb)
+        st, fb, _ = L.lorenz_verify(key, n, 0, nb, bad)
+        assert st == L.E_INTEGRITY and fb == min(flips)
 
 
 def test_c5_bench_batch_16_trials():
