@@ -2,12 +2,15 @@
 // lorenz_autocorrelation (include/lorenz.h): the FFT pass plans and launches of spectra.cuh.
 // A translation unit of its own so the FFT instantiations compile beside the chain kernels
 // (build.py).
+#include <cuda.h>
+#include <cudaTypedefs.h>  // PFN_cuTensorMapEncodeTiled (the driver entry point, fetched at run time)
 #include <cuda_runtime.h>
 #include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <mutex>
 #include <string>
 
 #include "../../include/lorenz.h"
@@ -157,6 +160,54 @@ bool four_step_spectrum(uint32_t H, uint32_t W, uint32_t M, double scale, double
   return cuda_ok(cudaGetLastError(), "fft col0 unpack");
 }
 
+// The TMA column pass (spectra.cuh fft_col_tma_kernel): a tensor map over the H x M double2
+// workspace seen as H rows of 2 M doubles, boxes of 256 rows x 2 doubles. cuTensorMapEncodeTiled is a
+// driver call; the runtime hands out its entry point (no link against libcuda).
+#ifndef LZ_COL_TMA
+#define LZ_COL_TMA 1
+#endif
+bool col_tensor_map(CUtensorMap* map, double2* ws, uint32_t H, uint32_t M) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    else
+      cudaGetLastError();
+  });
+  if (!encode) return false;
+  const cuuint64_t dims[2] = {2ull * M, H};
+  const cuuint64_t strides[1] = {(cuuint64_t)M * sizeof(double2)};
+  const cuuint32_t box[2] = {2, 256}, estr[2] = {1, 1};
+  return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, ws, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// the autocorrelation's fused column pass over M packed columns of H = 4096 with TMA; false (nothing
+// launched) when the tensor map cannot be built, and the caller runs fft_pass_kernel instead
+bool col_power_fft_tma(const lz::FftPass& cols, double2* ws, uint32_t H, uint32_t M, cudaStream_t st, bool* launched) {
+  *launched = false;
+  if (!LZ_COL_TMA || H != 4096) return true;
+  CUtensorMap map;
+  if (!col_tensor_map(&map, ws, H, M)) return true;
+  lz::FftPass c = cols;
+  c.S = 1;
+  c.logS = 0;
+  c.T = H / 16;
+  c.pitch = H + H / 16;
+  const size_t smem = (size_t)c.pitch * sizeof(double2) + 128;  // + alignment slack (TMA: 128-byte boxes)
+  auto kernel = lz::fft_col_tma_kernel<12>;
+  if (!cuda_ok(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "fft smem"))
+    return false;
+  kernel<<<M, 256, smem, st>>>(c, map);
+  *launched = true;
+  return cuda_ok(cudaGetLastError(), "fft column pass (TMA)");
+}
+
 lorenz_status spectra_args(const uint8_t* x, uint32_t H, uint32_t W, const double* out) {
   if (!x || !out || !fft_side(H) || !fft_side(W) || (reinterpret_cast<uintptr_t>(out) & 7)) {
     lz::set_last_error("H and W must be powers of two in [2, 4096]; x and out non-null device pointers, out 8-aligned");
@@ -256,8 +307,11 @@ lorenz_status lorenz_autocorrelation(const uint8_t* x, uint32_t H, uint32_t W, d
     lz::FftPass rows2 = fft_rows(H, M, M, M);
     rows1.W = cols.W = rows2.W = W;
     cols.packed0 = 1;
+    bool tma = false;
     ok = fft_launch<lz::FFT_IN_PAIRS_CENTRED, lz::FFT_OUT_R2C>(rows1, x, nullptr, ws, nullptr, aux, nullptr, st) &&
-         fft_launch<lz::FFT_IN_COMPLEX, lz::FFT_OUT_POWER_FFT>(cols, nullptr, ws, ws, nullptr, nullptr, nullptr, st) &&
+         col_power_fft_tma(cols, ws, H, M, st, &tma) &&
+         (tma || fft_launch<lz::FFT_IN_COMPLEX, lz::FFT_OUT_POWER_FFT>(cols, nullptr, ws, ws, nullptr, nullptr, nullptr,
+                                                                       st)) &&
          fft_launch<lz::FFT_IN_C2R, lz::FFT_OUT_REAL_PAIRS>(rows2, nullptr, ws, nullptr, r, aux, nullptr, st);
   } else if (ok) {
     const lz::FftPass rows1 = fft_rows(H, W, W, Pw), cols1 = fft_cols(H, W, Pw, Pw);

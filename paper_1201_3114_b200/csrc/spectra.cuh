@@ -18,6 +18,8 @@
 // 2..16-point DFTs use compile-time constants. At n = 4096: 3 passes, 2 exchanges.
 // HBM-bound: 16 B read + 16 B written per element per 1-D pass (bytes / doubles at the ends).
 #pragma once
+#include <cuda.h>  // CUtensorMap (fft_col_tma_kernel)
+
 #include <cstdint>
 
 namespace lz {
@@ -28,9 +30,10 @@ constexpr int kFftCtaThreads = 256;
 // FFT_IN_PAIRS_CENTRED: the same with the mean subtracted (exact).
 // FFT_IN_C2R: a Hermitian half spectrum Q[0..n] (Q[0] + i Q[n] packed in element 0, both real)
 //   pre-processed so that one n-point FFT yields the real 2n-point transform (see c2r_load).
+// FFT_IN_SMEM_DENSE: the tile is already in shared memory, unpadded (a TMA load; fft_col_tma_kernel).
 enum FftIn : int {
   FFT_IN_BYTES = 0, FFT_IN_CENTRED = 1, FFT_IN_COMPLEX = 2, FFT_IN_PAIRS = 3, FFT_IN_PAIRS_CENTRED = 4,
-  FFT_IN_C2R = 5
+  FFT_IN_C2R = 5, FFT_IN_SMEM_DENSE = 6
 };
 // FFT_OUT_R2C: unpack the row's half spectrum X[0..n] (2n-point real DFT) from the n-point complex
 //   FFT of the pairs, stored as n complex values with X[0] + i X[n] packed in element 0.
@@ -42,7 +45,8 @@ enum FftIn : int {
 //   exact lag-0 value (lag0_exact; r(0,0) = 1): the autocorrelation normalised in its last pass.
 enum FftOut : int {
   FFT_OUT_COMPLEX = 0, FFT_OUT_POWER = 1, FFT_OUT_SPECTRUM = 2, FFT_OUT_REAL = 3,
-  FFT_OUT_R2C = 4, FFT_OUT_HALF_SPECTRUM = 5, FFT_OUT_POWER_FFT = 6, FFT_OUT_REAL_PAIRS = 7
+  FFT_OUT_R2C = 4, FFT_OUT_HALF_SPECTRUM = 5, FFT_OUT_POWER_FFT = 6, FFT_OUT_REAL_PAIRS = 7,
+  FFT_OUT_SMEM = 8  // the last pass leaves the transform in shared memory, natural order, unpadded (for a TMA store)
 };
 
 struct FftPass {
@@ -207,7 +211,7 @@ struct FftIo {
   double* rout;
   double* lag0;
   double mean;
-  const double2* tlo;    // shared: exp(-2 pi i m / n), m < 64
+  const double2* tlo;    // shared: exp(-2 pi i m / n), m < 64, at tw_lo(m)
   const double2* thi;    // shared: exp(-2 pi i 64 m / n), m < n / 64
   const double2* t2lo;   // shared (R2C / C2R): exp(-2 pi i m / 2n), m < 64
   const double2* t2hi;   // shared (R2C / C2R): exp(-2 pi i 64 m / 2n), m < 2n / 64
@@ -231,11 +235,28 @@ __device__ __forceinline__ double2 twid2(const FftIo& io, uint32_t m) {  // exp(
   return cmul(io.t2lo[m & 63], io.t2hi[m >> 6]);
 }
 
-// exp(-2 pi i m / n) = tlo[m mod 64] * thi[m / 64] (n <= 4096: two 64-entry shared tables)
+// exp(-2 pi i m / n) = tlo[m mod 64] * thi[m / 64] (n <= 4096: two 64-entry shared tables). The low
+// table holds entry m at tw_lo(m) = m + m/8: a Stockham pass's twiddle steps are multiples of 8, 16
+// or 32 across a warp (pass 2 of a 2048-point row: m = 8 k), which in an unpadded table of 16-byte
+// entries all fall in one bank group (an 8-way conflict); one pad entry per 8 spreads them out.
+#ifndef LZ_TW_PAD
+#define LZ_TW_PAD 1
+#endif
+__host__ __device__ constexpr uint32_t tw_lo(uint32_t m) { return LZ_TW_PAD ? m + (m >> 3) : m; }
+constexpr uint32_t kTwLo = tw_lo(63) + 1;  // low-table entries (72 with the padding)
+template <int N>
+__host__ __device__ constexpr int tw_entries() { return (int)kTwLo + (N > 64 ? N / 64 : 1); }
+// every CTA fills its own tables from sincospi of exact dyadic arguments (twiddle_exact)
+template <int N>
+__device__ __forceinline__ void fill_twiddles(double2* tws, uint32_t t0, uint32_t nt) {
+  for (uint32_t i = t0; i < 64 + (N > 64 ? N / 64 : 0); i += nt)
+    if (i < 64) { if (i < (uint32_t)N) tws[tw_lo(i)] = twiddle_exact(i, N); }
+    else tws[kTwLo + i - 64] = twiddle_exact(64 * (i - 64), N);
+}
 template <int N>
 __device__ __forceinline__ double2 twid(const FftIo& io, uint32_t m) {
-  if (N <= 64) return io.tlo[m];
-  return cmul(io.tlo[m & 63], io.thi[m >> 6]);
+  if (N <= 64) return io.tlo[tw_lo(m)];
+  return cmul(io.tlo[tw_lo(m & 63)], io.thi[m >> 6]);
 }
 
 template <int IN, int N>
@@ -294,6 +315,53 @@ __device__ __forceinline__ void fft_store(const FftPass& p, const FftIo& io, uin
   }
 }
 
+#ifndef LZ_C2R_PAIRED
+#define LZ_C2R_PAIRED 1
+#endif
+// The C2R pre-processing done in registers (FFT_IN_C2R, first pass of radix R < 16: fft_passes then
+// runs the remainder radix first). The first pass gives thread tid the G/2 groups j = tid + g T and
+// their mirrors j' = NR - j (NR/2 for j = 0): the inputs l = j + t NR and N - l = j' + (R - 1 - t) NR
+// are then in the same thread, which loads Q[l] and Q[N - l] once each and forms V[l] and V[N - l]
+// from them (fft_load's formulas; exp(-2 pi i (N - l) / 2N) = -conj exp(-2 pi i l / 2N)). Measured
+// at 4096^2: the C2R row pass 107 -> 72 us. (The same pairing for the R2C unpacking in the last
+// pass measured slower, 70 -> 80 us, and is not used.)
+__device__ __forceinline__ double2 c2r_v(double2 a, double2 b, double2 w) {  // a = Q[l], b = Q[N - l]
+  const double2 ge = make_double2(__dmul_rn(__dadd_rn(a.x, b.x), 0.5), __dmul_rn(__dsub_rn(a.y, b.y), 0.5));
+  const double2 d = make_double2(__dmul_rn(__dsub_rn(a.x, b.x), 0.5), __dmul_rn(__dadd_rn(a.y, b.y), 0.5));
+  const double2 go = cmul(w, d);
+  return make_double2(__dadd_rn(ge.x, go.y), __dsub_rn(ge.y, go.x));  // ge - i go
+}
+template <int N>
+__device__ __forceinline__ void c2r_pair(const FftIo& io, double2& A, double2& B, uint32_t l) {
+  const double2 a = A, b = B, w = twid2<N>(io, l);
+  A = c2r_v(a, b, w);
+  B = c2r_v(b, a, make_double2(-w.x, w.y));
+}
+template <int R, int N>
+__device__ __forceinline__ void c2r_registers(const FftIo& io, double2 (&a)[16], uint32_t tid) {
+  constexpr int G = 16 / R, T = N / 16, NR = N / R;
+#pragma unroll
+  for (int g = 0; g < G / 2; ++g) {
+    const uint32_t j = tid + g * T;
+    const int gm = g + G / 2;
+    if (g > 0 || j != 0) {
+#pragma unroll
+      for (int t = 0; t < R; ++t) c2r_pair<N>(io, a[g * R + t], a[gm * R + R - 1 - t], j + t * NR);
+    } else {
+      const double2 q0 = a[0];  // Q[0] + i Q[N], both real
+      a[0] = make_double2(__dmul_rn(__dadd_rn(q0.x, q0.y), 0.5), __dmul_rn(__dsub_rn(q0.y, q0.x), 0.5));
+      {
+        const double2 h = a[R / 2];  // l = N/2 pairs with itself
+        a[R / 2] = c2r_v(h, h, twid2<N>(io, N / 2));
+      }
+#pragma unroll
+      for (int t = 1; t < R / 2; ++t) c2r_pair<N>(io, a[t], a[R - t], t * NR);
+#pragma unroll
+      for (int t = 0; t < R / 2; ++t) c2r_pair<N>(io, a[gm * R + t], a[gm * R + R - 1 - t], NR / 2 + t * NR);
+    }
+  }
+}
+
 // one Stockham pass of radix R after sub-transforms of length LS: group j (< N/R) takes
 // x[j + t N/R], t < R, multiplies by exp(-2 pi i t k / (LS R)), k = j mod LS, does the R-point
 // DFT and writes y_u to (j - k) R + k + u LS. Everything but the thread's indices is static.
@@ -305,22 +373,36 @@ __device__ __forceinline__ void fft_pass(const FftPass& p, const FftIo& io, doub
                                          uint32_t tid, uint64_t seq, bool active, bool valid, FlatAcc& acc,
                                          const Pre& pre) {
   constexpr int E = N < 16 ? N : 16, G = E / R, T = N / E, NR = N / R;
-  constexpr bool FROM_XS = !FIRST || (SMEM_SRC && IN == FFT_IN_COMPLEX);
+  constexpr bool FROM_XS = !FIRST || (SMEM_SRC && (IN == FFT_IN_COMPLEX || IN == FFT_IN_SMEM_DENSE));
+  // the unpadded tile of a TMA load / store is read by the first pass and written by the last one at
+  // consecutive indices across a warp (idx = j + t NR, pos = j + u LS): conflict-free without padding
+  constexpr bool DENSE_RD = FIRST && IN == FFT_IN_SMEM_DENSE, DENSE_WR = LAST && OUT == FFT_OUT_SMEM;
+  constexpr bool PAIRED_IN = LZ_C2R_PAIRED && FIRST && IN == FFT_IN_C2R && N > 16 && G >= 2;  // c2r_registers
+  // group g's j: tid + g T, or for PAIRED_IN's second half the mirror NR - j of the first half's j
+  // (NR/2 for j = 0), so that the thread holds the input at l and N - l together
+  auto jof = [&](int g) -> uint32_t {
+    if (!PAIRED_IN || g < G / 2) return tid + g * T;
+    const uint32_t jj = tid + (g - G / 2) * T;
+    return jj ? NR - jj : NR / 2;
+  };
 #pragma unroll
   for (int g = 0; g < G && active; ++g) {
-    const uint32_t j = tid + g * T;
+    const uint32_t j = jof(g);
 #pragma unroll
     for (int t = 0; t < R; ++t) {
       const uint32_t idx = j + t * NR;
-      if (!FROM_XS) a[g * R + t] = valid ? fft_load<IN, N>(p, io, seq, idx) : make_double2(0.0, 0.0);
-      else a[g * R + t] = Xs[fft_pad(idx)];
+      if (PAIRED_IN) a[g * R + t] = valid ? io.cin[seq * p.in_pitch + idx] : make_double2(0.0, 0.0);
+      else if (!FROM_XS) a[g * R + t] = valid ? fft_load<IN, N>(p, io, seq, idx) : make_double2(0.0, 0.0);
+      else a[g * R + t] = Xs[DENSE_RD ? idx : fft_pad(idx)];
     }
   }
+  if constexpr (PAIRED_IN)
+    if (active) c2r_registers<R, N>(io, a, tid);
   if (FROM_XS) __syncthreads();  // every read of this pass done before anyone overwrites the tile
   if (LAST) pre();
 #pragma unroll
   for (int g = 0; g < G && active; ++g) {
-    const uint32_t j = tid + g * T, k = j & (LS - 1);
+    const uint32_t j = jof(g), k = j & (LS - 1);
     if (LS > 1 && k) {
       // w^t for t < R from w, w^2, w^4, w^8 only: w^t = w^(t&3) * w^(t&12) (at most two extra
       // complex products per factor); each w^(2^i) is itself a product of two shared-table entries
@@ -346,14 +428,16 @@ __device__ __forceinline__ void fft_pass(const FftPass& p, const FftIo& io, doub
     for (int u = 0; u < R; ++u) {
       const uint32_t pos = (j - k) * R + k + u * LS;
       const double2 v = a[g * R + bitrev_c<R>(u)];
-      if (LAST && !(OUT == FFT_OUT_R2C || OUT == FFT_OUT_POWER_FFT || (OUT == FFT_OUT_HALF_SPECTRUM && seq == 0))) {
+      if (LAST && !(OUT == FFT_OUT_R2C || OUT == FFT_OUT_POWER_FFT || OUT == FFT_OUT_SMEM ||
+                    (OUT == FFT_OUT_HALF_SPECTRUM && seq == 0))) {
         if (valid) fft_store<OUT>(p, io, seq, pos, v, acc);
       } else {
-        Xs[fft_pad(pos)] = v;  // exchange, or the input of a shared-memory epilogue
+        Xs[DENSE_WR ? pos : fft_pad(pos)] = v;  // exchange, or the input of a shared-memory epilogue
       }
     }
   }
-  if (!LAST || OUT == FFT_OUT_R2C || OUT == FFT_OUT_HALF_SPECTRUM || OUT == FFT_OUT_POWER_FFT) __syncthreads();
+  if (!LAST || OUT == FFT_OUT_R2C || OUT == FFT_OUT_HALF_SPECTRUM || OUT == FFT_OUT_POWER_FFT || OUT == FFT_OUT_SMEM)
+    __syncthreads();
 }
 
 // the passes of an N = 2^LOGN transform: radix 16 while >= 4 bits remain, then the remainder
@@ -361,7 +445,9 @@ template <int LOGN, int DONE, int IN, int OUT, bool SMEM_SRC = false, typename P
 __device__ __forceinline__ void fft_passes(const FftPass& p, const FftIo& io, double2 (&a)[16], double2* Xs,
                                            uint32_t tid, uint64_t seq, bool active, bool valid, FlatAcc& acc,
                                            const Pre& pre) {
-  constexpr int REM = LOGN - DONE, RL = REM >= 4 ? 4 : REM;
+  // C2R input (c2r_registers) runs the remainder radix first, so that its first pass has >= 2 groups
+  constexpr bool REMF = LZ_C2R_PAIRED && IN == FFT_IN_C2R && LOGN > 4 && (LOGN & 3) != 0;
+  constexpr int REM = LOGN - DONE, RL = (REMF && DONE == 0) ? (LOGN & 3) : (REM >= 4 ? 4 : REM);
   fft_pass<1 << RL, 1 << LOGN, 1 << DONE, DONE == 0, REM == RL, IN, OUT, SMEM_SRC>(p, io, a, Xs, tid, seq, active,
                                                                                     valid, acc, pre);
   if constexpr (REM > RL)
@@ -480,11 +566,9 @@ __global__ void __launch_bounds__(CTA, 512 / CTA)
   const bool active = s < p.S && tid < (uint32_t)T;  // (a CTA narrower than 256 threads leaves some idle)
   const bool valid = active && seq < p.nseq;
   double2* Xs = fsm + (size_t)(active ? s : 0) * p.pitch;
-  __shared__ double2 tws[64 + (N > 64 ? N / 64 : 1)];
-  for (uint32_t i = threadIdx.x; i < 64 + (N > 64 ? N / 64 : 0); i += CTA)
-    if (i < 64) { if (i < (uint32_t)N) tws[i] = twiddle_exact(i, N); }
-    else tws[i] = twiddle_exact(64 * (i - 64), N);
-  FftIo io{bytes, nullptr, seq0, cin, cout, rout, lag0, 0.0, tws, tws + 64, nullptr, nullptr};
+  __shared__ double2 tws[tw_entries<N>()];
+  fill_twiddles<N>(tws, threadIdx.x, CTA);
+  FftIo io{bytes, nullptr, seq0, cin, cout, rout, lag0, 0.0, tws, tws + kTwLo, nullptr, nullptr};
   if (IN == FFT_IN_CENTRED || IN == FFT_IN_PAIRS_CENTRED)
     io.mean = __ddiv_rn((double)*sum, (double)p.H * (double)p.W);
   if (OUT == FFT_OUT_REAL_PAIRS) {
@@ -575,7 +659,7 @@ __global__ void __launch_bounds__(CTA, 512 / CTA)
   static_assert(N >= 256, "persistent FFT needs >= 2 passes");
   extern __shared__ double2 fsm[];
   __shared__ uint4 stage[CTA];
-  __shared__ double2 tws[64 + N / 64];
+  __shared__ double2 tws[tw_entries<N>()];
   uint32_t s, tid;
   if (p.rows) { s = threadIdx.x / T; tid = threadIdx.x % T; }
   else { s = threadIdx.x & (p.S - 1); tid = threadIdx.x >> p.logS; }
@@ -584,8 +668,8 @@ __global__ void __launch_bounds__(CTA, 512 / CTA)
   const uint64_t tiles = (p.nseq + p.S - 1) / p.S;
   uint64_t tile = blockIdx.x;
   if (tile < tiles) fft_prefetch<IN, N, LOGN, CTA>(p, bytes, cin, fsm, stage, tile);
-  for (uint32_t i = threadIdx.x; i < 64 + N / 64; i += CTA) tws[i] = twiddle_exact(i < 64 ? i : 64 * (i - 64), N);
-  FftIo io{bytes, reinterpret_cast<const uint8_t*>(stage), 0, cin, cout, rout, lag0, 0.0, tws, tws + 64};
+  fill_twiddles<N>(tws, threadIdx.x, CTA);
+  FftIo io{bytes, reinterpret_cast<const uint8_t*>(stage), 0, cin, cout, rout, lag0, 0.0, tws, tws + kTwLo};
   if (IN == FFT_IN_CENTRED) io.mean = __ddiv_rn((double)*sum, (double)p.H * (double)p.W);
   double2 a[16];
   FlatAcc fa;
@@ -604,6 +688,78 @@ __global__ void __launch_bounds__(CTA, 512 / CTA)
   if (OUT == FFT_OUT_SPECTRUM && p.part) flat_partial<CTA>(fa, p.part);
 }
 
+
+// ---------------------------------------------------------------- TMA column transform
+// The autocorrelation's fused column pass (FFT_OUT_POWER_FFT: transform, |.|^2, transform) for
+// H = 4096 with the Tensor Memory Accelerator: one column per 256-thread CTA, two CTAs per SM. The
+// column is read row segment by row segment, 16 bytes per row; plain loads cost the LSU one L1
+// wavefront per row (a warp's 32 rows = 32 wavefronts: the LSU-bound 2-column kernel), TMA moves
+// the same bytes without them. The tensor map views the workspace as H rows of 2 M doubles; a box is
+// 256 rows x one column (2 doubles = 16 bytes), 4 KB landing unpadded (TMA destinations are 128-byte
+// aligned) at tile offset 256 b, N/256 boxes per column completing on one mbarrier. The first pass
+// reads the unpadded tile (FFT_IN_SMEM_DENSE) and the exchanges after it use the padded layout; the
+// second transform's last pass writes the unpadded tile (FFT_OUT_SMEM) and the same boxes go back with
+// TMA stores. The 32-byte sectors a column half-uses are completed from L2 by the neighbouring
+// column's CTA, which runs beside it.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+      ::"r"(smem_u32(dst)), "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int c0, int c1, const void* src) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%1, %2}], [%3];"
+               ::"l"(map), "r"(c0), "r"(c1), "r"(smem_u32(src)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred P1;\n LAB_WAIT:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      " @P1 bra DONE;\n bra LAB_WAIT;\n DONE:\n}\n" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+
+template <int LOGN>
+__global__ void __launch_bounds__(256, 2) fft_col_tma_kernel(const FftPass p, const __grid_constant__ CUtensorMap map) {
+  constexpr int N = 1 << LOGN, T = N / 16, BOX = 256, NB = N / BOX;
+  static_assert(T == 256, "one column per 256-thread CTA");
+  extern __shared__ __align__(128) double2 fsm_raw[];  // N + N/16 elements (padded exchanges) + 128 B of slack
+  double2* fsm = reinterpret_cast<double2*>((reinterpret_cast<uintptr_t>(fsm_raw) + 127) & ~uintptr_t(127));
+  __shared__ double2 tws[tw_entries<N>()];
+  __shared__ __align__(8) uint64_t bar;
+  const uint32_t tid = threadIdx.x;
+  const uint64_t seq = blockIdx.x;
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid < 32) {  // warp 0 issues the column's N/BOX box loads
+    if (tid == 0)
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar)), "r"(N * 16)
+                   : "memory");
+    if (tid < (uint32_t)NB) tma_load_2d(fsm + BOX * tid, &map, 2 * (int)seq, BOX * (int)tid, &bar);
+  }
+  fill_twiddles<N>(tws, tid, 256);
+  __syncthreads();  // twiddle tables
+  mbar_wait(&bar, 0);
+  FftIo io{nullptr, nullptr, seq, nullptr, nullptr, nullptr, nullptr, 0.0, tws, tws + kTwLo, nullptr, nullptr};
+  double2 a[16];
+  FlatAcc fa;
+  fft_passes<LOGN, 0, FFT_IN_SMEM_DENSE, FFT_OUT_POWER_FFT, true>(p, io, a, fsm, tid, seq, true, true, fa,
+                                                                  no_prefetch);
+  power_in_place<N>(p, fsm, tid, seq, true);
+  __syncthreads();
+  fft_passes<LOGN, 0, FFT_IN_COMPLEX, FFT_OUT_SMEM, true>(p, io, a, fsm, tid, seq, true, true, fa, no_prefetch);
+  // (fft_pass ended with a barrier after the tile writes) generic-proxy writes -> the TMA engine
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+  if (tid < 32) {
+    if (tid < (uint32_t)NB) tma_store_2d(&map, 2 * (int)seq, BOX * (int)tid, fsm + BOX * tid);
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // the tile is read before the CTA exits
+  }
+}
 
 // ---------------------------------------------------------------- four-step column transform
 // The power spectrum's column transforms for H = 16 H2 (H = 2048, 4096): stage 1 below, then stage 2 =

@@ -8,7 +8,7 @@ Prints JSON lines:
     R2C rows + half-spectrum columns) / 58 N (autocorrelation: byte sum, R2C rows, fused
     transform-|.|^2-transform columns, C2R rows, normalisation) -> GB/s;
   * the CPU oracle (plain O(N^2) sums, one core) timed beside the GPU at --oracle-side (128);
-  * the Fig.3 / Fig.4 experiment at --fig x --fig: a synthetic plain image, its ciphertext
+  * the Fig.3 / Fig.4 experiment at --fig x --fig (0: skipped): a synthetic plain image, its ciphertext
     (FAST, the first N ciphertext bytes) and white noise -> byte entropy, spectral flatness,
     r(1,0), r(0,1), max off-origin |r|.
 """
@@ -97,6 +97,8 @@ def main():
         print(json.dumps({"what": "CPU oracle beside the GPU (plain O(N^2) definitions, 1 core)", "side": s,
                           "oracle_spectrum_s": round(cp, 3), "gpu_spectrum_ms": round(tp * 1e3, 4),
                           "oracle_autocorr_s": round(ca, 3), "gpu_autocorr_ms": round(ta * 1e3, 4)}))
+    if not a.fig:
+        return
     s = a.fig
     n = s * s
     plain = plain_image(s, s)
