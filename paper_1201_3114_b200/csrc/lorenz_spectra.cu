@@ -187,11 +187,11 @@ bool col_tensor_map(CUtensorMap* map, double2* ws, uint32_t H, uint32_t M) {
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// the autocorrelation's fused column pass over M packed columns of H = 4096 with TMA; false (nothing
-// launched) when the tensor map cannot be built, and the caller runs fft_pass_kernel instead
+// the autocorrelation's fused column pass over M packed columns of H = 2048 or 4096 rows with TMA; false
+// (nothing launched) when the tensor map cannot be built, and the caller runs fft_pass_kernel instead
 bool col_power_fft_tma(const lz::FftPass& cols, double2* ws, uint32_t H, uint32_t M, cudaStream_t st, bool* launched) {
   *launched = false;
-  if (!LZ_COL_TMA || H != 4096) return true;
+  if (!LZ_COL_TMA || (H != 4096 && H != 2048)) return true;
   CUtensorMap map;
   if (!col_tensor_map(&map, ws, H, M)) return true;
   lz::FftPass c = cols;
@@ -200,12 +200,14 @@ bool col_power_fft_tma(const lz::FftPass& cols, double2* ws, uint32_t H, uint32_
   c.T = H / 16;
   c.pitch = H + H / 16;
   const size_t smem = (size_t)c.pitch * sizeof(double2) + 128;  // + alignment slack (TMA: 128-byte boxes)
-  auto kernel = lz::fft_col_tma_kernel<12>;
-  if (!cuda_ok(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "fft smem"))
-    return false;
-  kernel<<<M, 256, smem, st>>>(c, map);
-  *launched = true;
-  return cuda_ok(cudaGetLastError(), "fft column pass (TMA)");
+  auto go = [&](auto kernel) {
+    if (!cuda_ok(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "fft smem"))
+      return false;
+    kernel<<<M, H / 16, smem, st>>>(c, map);
+    *launched = true;
+    return cuda_ok(cudaGetLastError(), "fft column pass (TMA)");
+  };
+  return H == 4096 ? go(lz::fft_col_tma_kernel<12>) : go(lz::fft_col_tma_kernel<11>);
 }
 
 lorenz_status spectra_args(const uint8_t* x, uint32_t H, uint32_t W, const double* out) {

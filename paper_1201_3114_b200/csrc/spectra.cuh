@@ -691,10 +691,10 @@ __global__ void __launch_bounds__(CTA, 512 / CTA)
 
 // ---------------------------------------------------------------- TMA column transform
 // The autocorrelation's fused column pass (FFT_OUT_POWER_FFT: transform, |.|^2, transform) for
-// H = 4096 with the Tensor Memory Accelerator: one column per 256-thread CTA, two CTAs per SM. The
-// column is read row segment by row segment, 16 bytes per row; plain loads cost the LSU one L1
-// wavefront per row (a warp's 32 rows = 32 wavefronts: the LSU-bound 2-column kernel), TMA moves
-// the same bytes without them. The tensor map views the workspace as H rows of 2 M doubles; a box is
+// H = 4096 (2048) with the Tensor Memory Accelerator: one column per 256 (128)-thread CTA, two (four)
+// CTAs per SM. The column is read row segment by row segment, 16 bytes per row; plain loads cost the
+// LSU one L1 wavefront per row (a warp's 32 rows = 32 wavefronts: the LSU-bound 2-column kernel), TMA
+// moves the same bytes without them. The tensor map views the workspace as H rows of 2 M doubles; a box is
 // 256 rows x one column (2 doubles = 16 bytes), 4 KB landing unpadded (TMA destinations are 128-byte
 // aligned) at tile offset 256 b, N/256 boxes per column completing on one mbarrier. The first pass
 // reads the unpadded tile (FFT_IN_SMEM_DENSE) and the exchanges after it use the padded layout; the
@@ -719,9 +719,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 }
 
 template <int LOGN>
-__global__ void __launch_bounds__(256, 2) fft_col_tma_kernel(const FftPass p, const __grid_constant__ CUtensorMap map) {
-  constexpr int N = 1 << LOGN, T = N / 16, BOX = 256, NB = N / BOX;
-  static_assert(T == 256, "one column per 256-thread CTA");
+__global__ void __launch_bounds__((1 << LOGN) / 16, 8192 / (1 << LOGN))
+    fft_col_tma_kernel(const FftPass p, const __grid_constant__ CUtensorMap map) {
+  constexpr int N = 1 << LOGN, T = N / 16, BOX = 256, NB = N / BOX;  // one column per T-thread CTA
+  static_assert(N == 2048 || N == 4096, "TMA column pass: 2048 or 4096 rows");
   extern __shared__ __align__(128) double2 fsm_raw[];  // N + N/16 elements (padded exchanges) + 128 B of slack
   double2* fsm = reinterpret_cast<double2*>((reinterpret_cast<uintptr_t>(fsm_raw) + 127) & ~uintptr_t(127));
   __shared__ double2 tws[tw_entries<N>()];
@@ -740,7 +741,7 @@ __global__ void __launch_bounds__(256, 2) fft_col_tma_kernel(const FftPass p, co
                    : "memory");
     if (tid < (uint32_t)NB) tma_load_2d(fsm + BOX * tid, &map, 2 * (int)seq, BOX * (int)tid, &bar);
   }
-  fill_twiddles<N>(tws, tid, 256);
+  fill_twiddles<N>(tws, tid, T);
   __syncthreads();  // twiddle tables
   mbar_wait(&bar, 0);
   FftIo io{nullptr, nullptr, seq, nullptr, nullptr, nullptr, nullptr, 0.0, tws, tws + kTwLo, nullptr, nullptr};
@@ -834,7 +835,8 @@ __global__ void __launch_bounds__(kFftCta) byte_sum_kernel(const uint8_t* __rest
   unsigned long long acc = 0, acc2 = 0;
   const uint64_t t0 = (uint64_t)blockIdx.x * kFftCta + threadIdx.x, step = (uint64_t)gridDim.x * kFftCta;
   if ((reinterpret_cast<uintptr_t>(x) & 15) == 0 && n % 16 == 0) {  // 16 bytes per load, SAD / dp4a sums
-    for (uint64_t i = t0; i < n / 16; i += step) {
+#pragma unroll 4
+    for (uint64_t i = t0; i < n / 16; i += step) {  // (unrolled: four independent 16-byte loads in flight)
       const uint4 v = __ldcs(reinterpret_cast<const uint4*>(x) + i);
       acc += __vsadu4(v.x, 0u) + __vsadu4(v.y, 0u) + __vsadu4(v.z, 0u) + __vsadu4(v.w, 0u);
       acc2 += __dp4a(v.x, v.x, 0u) + __dp4a(v.y, v.y, 0u) + __dp4a(v.z, v.z, 0u) + __dp4a(v.w, v.w, 0u);
@@ -850,9 +852,19 @@ __global__ void __launch_bounds__(kFftCta) byte_sum_kernel(const uint8_t* __rest
     acc += __shfl_xor_sync(0xffffffffu, acc, o);
     acc2 += __shfl_xor_sync(0xffffffffu, acc2, o);
   }
+  // the CTA's warps combined in shared memory, then one atomic per sum per CTA (one per warp queued
+  // ~9,500 same-address atomics at L2 and took 10 us even when the bytes sat in L2)
+  __shared__ unsigned long long red[2][kFftCta / 32];
   if ((threadIdx.x & 31) == 0) {
-    if (acc) atomicAdd(out, acc);
-    if (acc2) atomicAdd(out + 2, acc2);
+    red[0][threadIdx.x >> 5] = acc;
+    red[1][threadIdx.x >> 5] = acc2;
+  }
+  __syncthreads();
+  if (threadIdx.x < 2) {
+    unsigned long long t = 0;
+#pragma unroll
+    for (int w = 0; w < kFftCta / 32; ++w) t += red[threadIdx.x][w];
+    if (t) atomicAdd(out + 2 * threadIdx.x, t);
   }
 }
 
