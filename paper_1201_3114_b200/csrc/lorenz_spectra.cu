@@ -101,6 +101,7 @@ bool fft_launch(const lz::FftPass& p, const uint8_t* bytes, const double2* cin, 
     case 10:
       return persist ? go(lz::fft_persistent_kernel<IN, OUT, 10, 256>) : go(lz::fft_pass_kernel<IN, OUT, 10, 256>);
     case 11:
+      if (cta == 128 && !persist) return go(lz::fft_pass_kernel<IN, OUT, 11, 128>);
       return persist ? go(lz::fft_persistent_kernel<IN, OUT, 11, 256>) : go(lz::fft_pass_kernel<IN, OUT, 11, 256>);
     default:
       if (cta == 512)
@@ -115,9 +116,19 @@ bool fft_launch(const lz::FftPass& p, const uint8_t* bytes, const double2* cin, 
 // H = 16 H2 for H = 2048, 4096, with at least 8 packed columns.
 bool four_step_cols(uint32_t H, uint32_t M) { return (H == 2048 || H == 4096) && M >= 8; }
 
+// stage 2 at H2 = 256: 8 columns per 128-thread CTA (against 16 per 256: 4096^2 spectrum 0.189 -> 0.188 ms)
+#ifndef LZ_S2_CTA
+#define LZ_S2_CTA 128
+#endif
 lz::FftPass four_step_stage2(uint32_t H, uint32_t W, uint32_t M) {
   const uint32_t H2 = H / 16;
   lz::FftPass c = lz::fft_plan(H2, ilog2(H2), M, false);
+  if (LZ_S2_CTA == 128 && H2 == 256 && c.S == 16) {  // 8 columns per 128-thread CTA
+    c.S = 8;
+    c.logS = 3;
+    c.pitch = H2 + H2 / 16;
+    c.pitch += (1 - c.pitch % 8 + 8) % 8;  // pitch = 1 (mod 8): fft_plan's rule for 8 sequences per phase
+  }
   c.rows = 0;
   c.in_pitch = M;
   c.out_pitch = M;
@@ -145,14 +156,16 @@ bool four_step_spectrum(uint32_t H, uint32_t W, uint32_t M, double scale, double
   if (!cuda_ok(cudaGetLastError(), "fft stage 1")) return false;
   const size_t smem = lz::fft_smem_bytes(c, true);
   const dim3 g2((c.nseq + c.S - 1) / c.S, 16);
-  auto go = [&](auto kernel) {
+  auto go = [&](auto kernel, unsigned cta) {
     if (!cuda_ok(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "fft smem"))
       return false;
-    kernel<<<g2, 256, smem, st>>>(c, nullptr, ws, nullptr, power, nullptr, nullptr);
+    kernel<<<g2, cta, smem, st>>>(c, nullptr, ws, nullptr, power, nullptr, nullptr);
     return cuda_ok(cudaGetLastError(), "fft stage 2");
   };
-  const bool ok = H2 == 256 ? go(lz::fft_pass_kernel<lz::FFT_IN_COMPLEX, lz::FFT_OUT_HALF_SPECTRUM, 8, 256>)
-                            : go(lz::fft_pass_kernel<lz::FFT_IN_COMPLEX, lz::FFT_OUT_HALF_SPECTRUM, 7, 256>);
+  const bool ok =
+      H2 == 256 ? (c.S == 8 ? go(lz::fft_pass_kernel<lz::FFT_IN_COMPLEX, lz::FFT_OUT_HALF_SPECTRUM, 8, 128>, 128)
+                            : go(lz::fft_pass_kernel<lz::FFT_IN_COMPLEX, lz::FFT_OUT_HALF_SPECTRUM, 8, 256>, 256))
+                : go(lz::fft_pass_kernel<lz::FFT_IN_COMPLEX, lz::FFT_OUT_HALF_SPECTRUM, 7, 256>, 256);
   if (!ok) return false;
   const unsigned g3 = H / 256;
   lz::col0_unpack_kernel<256><<<g3, 256, 0, st>>>(c, col0, power, part ? part + g2.x * g2.y : nullptr);

@@ -73,8 +73,16 @@ struct FftPass {
 };
 
 // CTA threads: 256, except 512 for 4096-point column passes (S = 2 adjacent columns per CTA,
-// so every 32-byte sector a warp touches is fully used)
-inline uint32_t fft_cta(uint32_t n, bool rows) { return (!rows && n >= 4096) ? 512 : 256; }
+// so every 32-byte sector a warp touches is fully used) and 128 for 2048-point row passes
+// 2048-point row passes (W = 4096): one row per 128-thread CTA, four CTAs per SM (measured against two
+// rows per 256-thread CTA: 4096^2 spectrum 0.189 -> 0.184 ms, autocorrelation 0.259 -> 0.253 ms)
+#ifndef LZ_ROW_CTA
+#define LZ_ROW_CTA 128
+#endif
+inline uint32_t fft_cta(uint32_t n, bool rows) {
+  if (rows && n >= 2048) return LZ_ROW_CTA;
+  return (!rows && n >= 4096) ? 512 : 256;
+}
 
 inline FftPass fft_plan(uint32_t n, uint32_t logn, uint32_t nseq, bool rows) {
   FftPass p{};
@@ -576,7 +584,7 @@ __global__ void __launch_bounds__(CTA, 512 / CTA)
     io.inv_c0 = io.c0 > 0.0 ? __drcp_rn(io.c0) : 0.0;
   }
   if constexpr ((IN == FFT_IN_BYTES || IN == FFT_IN_CENTRED || IN == FFT_IN_PAIRS || IN == FFT_IN_PAIRS_CENTRED) &&
-                N >= 16 && CTA == 256) {
+                N >= 16) {
     constexpr int BPE = (IN == FFT_IN_PAIRS || IN == FFT_IN_PAIRS_CENTRED) ? 2 : 1;  // bytes per element
     __shared__ uint4 stage[CTA * BPE];                // S N BPE = CTA * 16 * BPE bytes
     if (p.rows && p.in_pitch == (uint64_t)N * BPE && (reinterpret_cast<uintptr_t>(bytes) & 15) == 0) {
