@@ -194,3 +194,24 @@ def test_tall_matrices_sampled(h, w):
             assert abs(r[k, l] - oracle.autocorr_at(x, int(k), int(l))) <= tol_autocorr(x.size), (k, l)
     assert math.isclose(p.sum(), float((x.astype(np.float64) ** 2).mean()), rel_tol=1e-11)
     assert r[0, 0] == pytest.approx(1.0, abs=1e-13)
+
+
+@pytest.mark.parametrize("h,w", [(4096, 64), (2048, 128)])
+def test_tma_column_pass_is_the_one_that_runs(h, w):
+    """The autocorrelation's column pass at H = 2048 / 4096 is the TMA kernel (fft_col_tma_kernel), not
+    the fft_pass_kernel fallback the library keeps for when no tensor map can be built: the kernel
+    names CUPTI records for one call, and the result against the oracle at sampled lags."""
+    x = cipher_image(h, w, seed=h + 3 * w)
+    xd = torch.from_numpy(np.ascontiguousarray(x)).to(DEV)
+    r = torch.empty((h, w), dtype=torch.float64, device=DEV)
+    L.lorenz_autocorrelation(xd, r)  # warm (tensor-map encoder fetched, kernels loaded)
+    torch.cuda.synchronize()
+    with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA]) as prof:
+        L.lorenz_autocorrelation(xd, r)
+        torch.cuda.synchronize()
+    names = [e.name for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
+    assert any("fft_col_tma_kernel" in n for n in names), names
+    assert not any("fft_pass_kernel<2, 6" in n for n in names), names  # (IN_COMPLEX, OUT_POWER_FFT fallback)
+    rc = r.cpu().numpy()
+    for u, v in [(0, 0), (1, 0), (0, 1), (h - 1, w - 1), (h // 2, 3), (17, w // 2)]:
+        assert abs(rc[u, v] - oracle.autocorr_at(x, u, v)) <= tol_autocorr(x.size), (u, v)
