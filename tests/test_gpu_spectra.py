@@ -80,9 +80,10 @@ def structured(kind, h, w):
     return inputs.message(h * w, seed=17).reshape(h, w)
 
 
-# W = 64, 256, 128, 2048: the row passes' last (R2C) / first (C2R) radix is 2, 8, 4, 4 -> the
-# register-paired unpacking with 8, 2, 4, 4 groups per thread (spectra.cuh r2c_registers / c2r_registers)
-SHAPES = [(2, 2), (2, 8), (8, 2), (4, 16), (16, 32), (64, 64), (128, 32), (32, 256), (16, 128), (4, 2048)]
+# W = 64, 256, 128, 1024, 2048: the C2R row pass's first radix is 2, 8, 4, 2, 4 -> its register-paired
+# pre-processing with 8, 2, 4, 8, 4 groups per thread (spectra.cuh c2r_registers)
+SHAPES = [(2, 2), (2, 8), (8, 2), (4, 16), (16, 32), (64, 64), (128, 32), (32, 256), (16, 128), (8, 1024),
+          (4, 2048)]
 
 
 @pytest.mark.parametrize("shape", SHAPES)
