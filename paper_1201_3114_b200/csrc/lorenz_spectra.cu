@@ -140,10 +140,10 @@ lz::FftPass four_step_stage2(uint32_t H, uint32_t W, uint32_t M) {
   return c;
 }
 
-// stage 1 -> stage 2 (16 blocks of H2 rows) -> the packed column's unpacking; *nparts = flatness
-// partials written (stage 2's CTAs, then the unpacking's one)
+// stage 1 -> stage 2 (16 blocks of H2 rows) -> the packed column's unpacking, whose last CTA combines the
+// flatness partials (stage 2's CTAs, then the unpacking's) when flatness != null
 bool four_step_spectrum(uint32_t H, uint32_t W, uint32_t M, double scale, double2* ws, double2* col0,
-                        double* power, double2* part, cudaStream_t st, unsigned* nparts) {
+                        double* power, double2* part, unsigned* ctr, double* flatness, cudaStream_t st) {
   const uint32_t H2 = H / 16;
   lz::FftPass c = four_step_stage2(H, W, M);
   c.scale = scale;
@@ -151,8 +151,8 @@ bool four_step_spectrum(uint32_t H, uint32_t W, uint32_t M, double scale, double
   c.col0_out = col0;
   lz::FftPass s1 = c;
   const dim3 g1(H2 / 32, (M + 7) / 8);
-  if (H == 4096) lz::fft_col_stage1_kernel<12><<<g1, 256, 0, st>>>(s1, ws);
-  else lz::fft_col_stage1_kernel<11><<<g1, 256, 0, st>>>(s1, ws);
+  if (H == 4096) lz::fft_col_stage1_kernel<12><<<g1, 256, 0, st>>>(s1, ws, ctr);
+  else lz::fft_col_stage1_kernel<11><<<g1, 256, 0, st>>>(s1, ws, ctr);
   if (!cuda_ok(cudaGetLastError(), "fft stage 1")) return false;
   const size_t smem = lz::fft_smem_bytes(c, true);
   const dim3 g2((c.nseq + c.S - 1) / c.S, 16);
@@ -168,8 +168,8 @@ bool four_step_spectrum(uint32_t H, uint32_t W, uint32_t M, double scale, double
                 : go(lz::fft_pass_kernel<lz::FFT_IN_COMPLEX, lz::FFT_OUT_HALF_SPECTRUM, 7, 256>, 256);
   if (!ok) return false;
   const unsigned g3 = H / 256;
-  lz::col0_unpack_kernel<256><<<g3, 256, 0, st>>>(c, col0, power, part ? part + g2.x * g2.y : nullptr);
-  *nparts = g2.x * g2.y + g3;
+  lz::col0_unpack_kernel<256><<<g3, 256, 0, st>>>(c, col0, power, part ? part + g2.x * g2.y : nullptr, ctr, part,
+                                                  g2.x * g2.y + g3, (uint64_t)H * W - 1, flatness);
   return cuda_ok(cudaGetLastError(), "fft col0 unpack");
 }
 
@@ -261,15 +261,17 @@ lorenz_status lorenz_power_spectrum(const uint8_t* x, uint32_t H, uint32_t W, do
     tiles = 16 * ((c2.nseq + c2.S - 1) / c2.S) + H / 256;
   }
   unsigned nparts = 0;  // one flatness partial per column CTA
-  bool ok = !flatness ||
-            cuda_ok(lz::lib_malloc_async(reinterpret_cast<void**>(&part), tiles * sizeof(double2), st), "alloc");
+  // (+ 16 bytes: the four-step's CTA counter)
+  bool ok = !flatness || cuda_ok(lz::lib_malloc_async(reinterpret_cast<void**>(&part), (tiles + 1) * sizeof(double2), st),
+                                 "alloc");
   double2* col0 = nullptr;  // the four-step's packed column U[k]
   ok = ok && (!four || cuda_ok(lz::lib_malloc_async(reinterpret_cast<void**>(&col0), H * sizeof(double2), st), "alloc"));
   cols.part = flatness ? part : nullptr;
   if (four)
     ok = ok &&
          fft_launch<lz::FFT_IN_PAIRS, lz::FFT_OUT_R2C>(rows, x, nullptr, ws, nullptr, nullptr, nullptr, st) &&
-         four_step_spectrum(H, W, M, cols.scale, ws, col0, power, cols.part, st, &nparts);
+         four_step_spectrum(H, W, M, cols.scale, ws, col0, power, cols.part,
+                            part ? reinterpret_cast<unsigned*>(part + tiles) : nullptr, flatness, st);
   else if (r2c)
     ok = ok &&
          fft_launch<lz::FFT_IN_PAIRS, lz::FFT_OUT_R2C>(rows, x, nullptr, ws, nullptr, nullptr, nullptr, st) &&
@@ -280,7 +282,7 @@ lorenz_status lorenz_power_spectrum(const uint8_t* x, uint32_t H, uint32_t W, do
          fft_launch<lz::FFT_IN_BYTES, lz::FFT_OUT_COMPLEX>(rows, x, nullptr, ws, nullptr, nullptr, nullptr, st) &&
          fft_launch<lz::FFT_IN_COMPLEX, lz::FFT_OUT_SPECTRUM>(cols, nullptr, ws, ws, power, nullptr, nullptr, st,
                                                               &nparts);
-  if (ok && flatness) {
+  if (ok && flatness && !four) {  // (the four-step path's col0_unpack_kernel combines them)
     lz::flatness_final_kernel<<<1, lz::kFftCta, 0, st>>>(part, nparts, N - 1, flatness);
     ok = cuda_ok(cudaGetLastError(), "flatness");
   }

@@ -25,6 +25,7 @@
 namespace lz {
 
 constexpr int kFftCtaThreads = 256;
+constexpr int kFftCta = 256;  // the reductions (byte sums, flatness, col0 unpacking)
 
 // FFT_IN_PAIRS: a real row of 2n bytes read as n complex values x[2m] + i x[2m+1] (real-to-complex)
 // FFT_IN_PAIRS_CENTRED: the same with the mean subtracted (exact).
@@ -484,6 +485,30 @@ __device__ __forceinline__ void flat_partial(const FlatAcc& fa, double2* part) {
   }
 }
 
+// spectral flatness = exp(mean log P) / mean P over the non-DC bins, from the per-CTA partials
+// of the spectrum's column pass, combined in index order (deterministic: same bits every run) by one
+// kFftCta-thread CTA (flatness_final_kernel, or the last CTA of col0_unpack_kernel)
+__device__ __forceinline__ void flatness_combine(const double2* part, uint32_t nparts, uint64_t bins, double* out) {
+  __shared__ double2 red[kFftCta];
+  double sl = 0.0, sp = 0.0;
+  for (uint32_t b = threadIdx.x; b < nparts; b += kFftCta) {  // fixed assignment and order
+    const double2 v = __ldcg(part + b);                        // (L2: partials of other CTAs)
+    sl = __dadd_rn(sl, v.x);
+    sp = __dadd_rn(sp, v.y);
+  }
+  red[threadIdx.x] = make_double2(sl, sp);
+  __syncthreads();
+  for (int h = kFftCta / 2; h > 0; h >>= 1) {
+    if ((int)threadIdx.x < h)
+      red[threadIdx.x] = make_double2(__dadd_rn(red[threadIdx.x].x, red[threadIdx.x + h].x),
+                                      __dadd_rn(red[threadIdx.x].y, red[threadIdx.x + h].y));
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double M = (double)bins;
+    *out = red[0].y == 0.0 ? 0.0 : __ddiv_rn(exp(__ddiv_rn(red[0].x, M)), __ddiv_rn(red[0].y, M));
+  }
+}
 // FFT_OUT_R2C epilogue: Z = the n-point FFT of z[m] = x[2m] + i x[2m+1] is in Xs (natural order).
 // With a = Z[l], b = conj(Z[n-l]): Fe = (a + b)/2, Fo = -i (a - b)/2, w = exp(-2 pi i l / 2n):
 // X[l] = Fe + w Fo and X[n-l] = conj(Fe - w Fo); X[0] = Re Z0 + Im Z0 and X[n] = Re Z0 - Im Z0 are
@@ -781,8 +806,9 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, 8192 / (1 << LOGN))
 // rows per k1, 16 columns per CTA, and writes P at rows k1 + 16 k2. The single-pass alternative moves
 // 32-byte row segments of 2 columns and is bound by the LSU.
 template <int LOGN>
-__global__ void __launch_bounds__(256) fft_col_stage1_kernel(const FftPass p, double2* __restrict__ ws) {
+__global__ void __launch_bounds__(256) fft_col_stage1_kernel(const FftPass p, double2* __restrict__ ws, unsigned* ctr) {
   constexpr int N = 1 << LOGN, N2 = N / 16;
+  if (ctr && (blockIdx.x | blockIdx.y | threadIdx.x) == 0) *ctr = 0;  // col0_unpack_kernel's CTA counter
   __shared__ double2 tw[64 + N / 64];
   for (uint32_t i = threadIdx.x; i < 64 + N / 64; i += 256) tw[i] = twiddle_exact(i < 64 ? i : 64 * (i - 64), N);
   __syncthreads();
@@ -811,10 +837,15 @@ __global__ void __launch_bounds__(256) fft_col_stage1_kernel(const FftPass p, do
 }
 
 // The packed DC / Nyquist column after stage 2 (U[k] gathered from the 16 k1 blocks): the same
-// unpacking as half_col0_epilogue; CTA b's flatness partial goes to part[b].
+// unpacking as half_col0_epilogue; CTA b's flatness partial goes to part[b]. With flat != null the
+// last CTA to finish (a counter stage 1 zeroed) combines all nparts partials from all_parts into the
+// flatness (flatness_combine: the same order and bits as flatness_final_kernel, one launch fewer).
 template <int CTA>
 __global__ void __launch_bounds__(CTA) col0_unpack_kernel(const FftPass p, const double2* __restrict__ u,
-                                                          double* __restrict__ rout, double2* part) {
+                                                          double* __restrict__ rout, double2* part, unsigned* ctr,
+                                                          const double2* all_parts, uint32_t nparts, uint64_t bins,
+                                                          double* flat) {
+  static_assert(CTA == kFftCta, "flatness_combine runs on this CTA");
   FlatAcc fa;
   const uint32_t N = p.H;
   for (uint32_t k = blockIdx.x * CTA + threadIdx.x; k < N; k += CTA * gridDim.x) {
@@ -832,9 +863,20 @@ __global__ void __launch_bounds__(CTA) col0_unpack_kernel(const FftPass p, const
     }
   }
   if (part) flat_partial<CTA>(fa, part);
+  if (flat) {
+    __shared__ bool last;
+    if (threadIdx.x == 0) {
+      __threadfence();  // this CTA's partial visible before it is counted
+      last = atomicAdd(ctr, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last) {
+      __threadfence();
+      flatness_combine(all_parts, nparts, bins, flat);
+    }
+  }
 }
 
-constexpr int kFftCta = 256;  // the reductions below
 
 // sum of the H*W bytes (the mean of the autocorrelation's centring; < 2^36, exact) in out[0] and
 // the sum of their squares (< 2^44, exact) in out[2]
@@ -892,28 +934,10 @@ __global__ void __launch_bounds__(kFftCta) autocorr_normalise_kernel(double* __r
   }
 }
 
-// spectral flatness = exp(mean log P) / mean P over the non-DC bins, from the per-CTA partials
-// of the spectrum's column pass, combined in index order (deterministic: same bits every run)
+// spectral flatness: see flatness_combine
 __global__ void __launch_bounds__(kFftCta) flatness_final_kernel(const double2* __restrict__ part, uint32_t nparts,
                                                                  uint64_t bins, double* __restrict__ out) {
-  __shared__ double2 red[kFftCta];
-  double sl = 0.0, sp = 0.0;
-  for (uint32_t b = threadIdx.x; b < nparts; b += kFftCta) {  // fixed assignment and order
-    sl = __dadd_rn(sl, part[b].x);
-    sp = __dadd_rn(sp, part[b].y);
-  }
-  red[threadIdx.x] = make_double2(sl, sp);
-  __syncthreads();
-  for (int h = kFftCta / 2; h > 0; h >>= 1) {
-    if ((int)threadIdx.x < h)
-      red[threadIdx.x] = make_double2(__dadd_rn(red[threadIdx.x].x, red[threadIdx.x + h].x),
-                                      __dadd_rn(red[threadIdx.x].y, red[threadIdx.x + h].y));
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    const double M = (double)bins;
-    *out = red[0].y == 0.0 ? 0.0 : __ddiv_rn(exp(__ddiv_rn(red[0].x, M)), __ddiv_rn(red[0].y, M));
-  }
+  flatness_combine(part, nparts, bins, out);
 }
 
 }  // namespace lz
