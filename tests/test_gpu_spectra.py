@@ -71,6 +71,10 @@ def structured(kind, h, w):
         return (255 * ((i + j) % 2)).astype(np.uint8)
     if kind == "constant":
         return np.full((h, w), 91, dtype=np.uint8)
+    if kind == "near_constant":  # large mean, tiny variance: the autocorrelation's centring must be exact
+        x = np.full((h, w), 200, dtype=np.uint8)
+        x[h // 3, (2 * w) // 3] = 201
+        return x
     if kind == "impulse":
         x = np.zeros((h, w), dtype=np.uint8)
         x[h - 1, w // 3] = 255
@@ -104,7 +108,7 @@ def test_power_spectrum_parity(shape, kind):
 
 
 @pytest.mark.parametrize("shape", SHAPES)
-@pytest.mark.parametrize("kind", ["noise", "plain", "checker", "impulse", "constant"])
+@pytest.mark.parametrize("kind", ["noise", "plain", "checker", "impulse", "constant", "near_constant"])
 def test_autocorrelation_parity(shape, kind):
     x = structured(kind, *shape)
     r = gpu_autocorr(x)
@@ -216,3 +220,17 @@ def test_tma_column_pass_is_the_one_that_runs(h, w):
     rc = r.cpu().numpy()
     for u, v in [(0, 0), (1, 0), (0, 1), (h - 1, w - 1), (h // 2, 3), (17, w // 2)]:
         assert abs(rc[u, v] - oracle.autocorr_at(x, u, v)) <= tol_autocorr(x.size), (u, v)
+
+
+def test_near_constant_full_size_closed_form():
+    """4096 x 4096 of 200 with one pixel of 201 (mean 200 + 1/N, variance ~1/N): the whole r matrix against
+    its closed form r = -1/(N-1) off the origin (any single-pixel deviation from a constant gives it). The
+    large mean makes this the case where the centring has to be exact before the transforms."""
+    h = w = 4096
+    n = h * w
+    x = structured("near_constant", h, w)
+    r = gpu_autocorr(x)
+    off = np.ones((h, w), dtype=bool)
+    off[0, 0] = False
+    assert r[0, 0] == 1.0
+    assert np.abs(r[off] + 1.0 / (n - 1)).max() <= tol_autocorr(n)
