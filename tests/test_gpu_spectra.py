@@ -234,3 +234,22 @@ def test_near_constant_full_size_closed_form():
     off[0, 0] = False
     assert r[0, 0] == 1.0
     assert np.abs(r[off] + 1.0 / (n - 1)).max() <= tol_autocorr(n)
+
+
+def test_full_size_every_bin_against_numpy_fft():
+    """4096 x 4096 ciphertext: EVERY frequency and lag (not a sample) against numpy's FFT in float64 — a
+    different algorithm (pocketfft), the route the oracle's own pins use (test_oracle_analysis.py) — within
+    the same FP64 bounds; the four-step spectrum, the TMA column pass and the paired C2R rows at full size."""
+    h = w = 4096
+    x = cipher_image(h, w, seed=21)
+    n = x.size
+    p, _ = gpu_spectrum(x)
+    xf = x.astype(np.float64)
+    want_p = np.fft.fftshift(np.abs(np.fft.fft2(xf)) ** 2) / float(n) ** 2
+    assert np.abs(p - want_p).max() <= tol_power(x)
+    del want_p
+    r = gpu_autocorr(x)
+    d = xf - xf.mean()
+    c = np.fft.ifft2(np.abs(np.fft.fft2(d)) ** 2).real
+    want_r = c / c[0, 0]
+    assert np.abs(r - want_r).max() <= tol_autocorr(n)
