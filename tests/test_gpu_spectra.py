@@ -236,12 +236,13 @@ def test_near_constant_full_size_closed_form():
     assert np.abs(r[off] + 1.0 / (n - 1)).max() <= tol_autocorr(n)
 
 
-def test_full_size_every_bin_against_numpy_fft():
-    """4096 x 4096 ciphertext: EVERY frequency and lag (not a sample) against numpy's FFT in float64 — a
-    different algorithm (pocketfft), the route the oracle's own pins use (test_oracle_analysis.py) — within
-    the same FP64 bounds; the four-step spectrum, the TMA column pass and the paired C2R rows at full size."""
-    h = w = 4096
-    x = cipher_image(h, w, seed=21)
+@pytest.mark.parametrize("h,w", [(4096, 4096), (2048, 2048), (4096, 64), (2048, 128), (1024, 4096)])
+def test_full_size_every_bin_against_numpy_fft(h, w):
+    """Ciphertext images up to 4096 x 4096: EVERY frequency and lag (not a sample) against numpy's FFT in
+    float64 — a different algorithm (pocketfft), the route the oracle's own pins use
+    (test_oracle_analysis.py) — within the same FP64 bounds; the four-step spectrum, the TMA column pass
+    (H = 2048, 4096) and the paired C2R rows at full size."""
+    x = cipher_image(h, w, seed=21 + h + w)
     n = x.size
     p, _ = gpu_spectrum(x)
     xf = x.astype(np.float64)
