@@ -47,7 +47,8 @@ enum FftIn : int {
 enum FftOut : int {
   FFT_OUT_COMPLEX = 0, FFT_OUT_POWER = 1, FFT_OUT_SPECTRUM = 2, FFT_OUT_REAL = 3,
   FFT_OUT_R2C = 4, FFT_OUT_HALF_SPECTRUM = 5, FFT_OUT_POWER_FFT = 6, FFT_OUT_REAL_PAIRS = 7,
-  FFT_OUT_SMEM = 8  // the last pass leaves the transform in shared memory, natural order, unpadded (for a TMA store)
+  FFT_OUT_SMEM = 8,  // the last pass leaves the transform in shared memory, natural order, unpadded (for a TMA store)
+  FFT_OUT_POWER_SMEM = 9  // the last pass leaves |X|^2 (as (P, 0)) in the exchange tile: power_in_place fused
 };
 
 struct FftPass {
@@ -437,15 +438,19 @@ __device__ __forceinline__ void fft_pass(const FftPass& p, const FftIo& io, doub
     for (int u = 0; u < R; ++u) {
       const uint32_t pos = (j - k) * R + k + u * LS;
       const double2 v = a[g * R + bitrev_c<R>(u)];
-      if (LAST && !(OUT == FFT_OUT_R2C || OUT == FFT_OUT_POWER_FFT || OUT == FFT_OUT_SMEM ||
+      if (LAST && !(OUT == FFT_OUT_R2C || OUT == FFT_OUT_POWER_FFT || OUT == FFT_OUT_SMEM || OUT == FFT_OUT_POWER_SMEM ||
                     (OUT == FFT_OUT_HALF_SPECTRUM && seq == 0))) {
         if (valid) fft_store<OUT>(p, io, seq, pos, v, acc);
       } else {
-        Xs[DENSE_WR ? pos : fft_pad(pos)] = v;  // exchange, or the input of a shared-memory epilogue
+        if (LAST && OUT == FFT_OUT_POWER_SMEM)
+          Xs[fft_pad(pos)] = make_double2(__dadd_rn(__dmul_rn(v.x, v.x), __dmul_rn(v.y, v.y)), 0.0);
+        else
+          Xs[DENSE_WR ? pos : fft_pad(pos)] = v;  // exchange, or the input of a shared-memory epilogue
       }
     }
   }
-  if (!LAST || OUT == FFT_OUT_R2C || OUT == FFT_OUT_HALF_SPECTRUM || OUT == FFT_OUT_POWER_FFT || OUT == FFT_OUT_SMEM)
+  if (!LAST || OUT == FFT_OUT_R2C || OUT == FFT_OUT_HALF_SPECTRUM || OUT == FFT_OUT_POWER_FFT || OUT == FFT_OUT_SMEM ||
+      OUT == FFT_OUT_POWER_SMEM)
     __syncthreads();
 }
 
@@ -780,10 +785,19 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, 8192 / (1 << LOGN))
   FftIo io{nullptr, nullptr, seq, nullptr, nullptr, nullptr, nullptr, 0.0, tws, tws + kTwLo, nullptr, nullptr};
   double2 a[16];
   FlatAcc fa;
-  fft_passes<LOGN, 0, FFT_IN_SMEM_DENSE, FFT_OUT_POWER_FFT, true>(p, io, a, fsm, tid, seq, true, true, fa,
-                                                                  no_prefetch);
-  power_in_place<N>(p, fsm, tid, seq, true);
-  __syncthreads();
+#ifndef LZ_TMA_FUSED_POWER
+#define LZ_TMA_FUSED_POWER 1
+#endif
+  // H = 4096 (121 -> 114 us); at 2048 rows the fused form measured no faster and is not compiled
+  if (seq == 0 || !LZ_TMA_FUSED_POWER || LOGN != 12) {  // packed DC / Nyquist column: |A|^2, |B|^2 need X[k], X[-k]
+    fft_passes<LOGN, 0, FFT_IN_SMEM_DENSE, FFT_OUT_POWER_FFT, true>(p, io, a, fsm, tid, seq, true, true, fa,
+                                                                    no_prefetch);
+    power_in_place<N>(p, fsm, tid, seq, true);
+    __syncthreads();
+  } else {  // every other column: |X[k]|^2 elementwise, written by the last pass itself
+    fft_passes<LOGN, 0, FFT_IN_SMEM_DENSE, FFT_OUT_POWER_SMEM, true>(p, io, a, fsm, tid, seq, true, true, fa,
+                                                                     no_prefetch);
+  }
   fft_passes<LOGN, 0, FFT_IN_COMPLEX, FFT_OUT_SMEM, true>(p, io, a, fsm, tid, seq, true, true, fa, no_prefetch);
   // (fft_pass ended with a barrier after the tile writes) generic-proxy writes -> the TMA engine
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
